@@ -1,0 +1,465 @@
+#!/usr/bin/env python3
+"""Benchmark: Z_p-RAID encode + 2-erasure recovery on B200 (libraid6c, sm_100a kernels).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path over one batch of synthetic stripes already
+resident in HBM: encode every stripe (P, Q), then rebuild an erasure pair in every stripe
+(per-stripe pairs cycling over all C(N+2,2) pairs, i.e. every class DD/DP/DQ/PQ), in place.
+Default workload = BASELINE.json configs[1] (c2): p=13, N=12, 4 MiB strips, 256 stripes
+per GPU (weak scaling: every rank owns its own 256 stripes; no data-path collective).
+
+metric value = user-data GB/s of the whole job = G * 2 * N * bytes * stripes / max-rank time
+(encode and recovery each process the stripe's N user strips once).  Inputs (14 GiB) are
+> 100x L2, so no L2 flush is needed between steps.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # cfg: p, N, strip bytes, stripes per GPU per step, sparse_mode, ops
+    1: dict(p=5, N=4, nbytes=64 << 10, stripes=4096, sparse=0, ops="enc+rec",
+            desc="c1 batched: p=5 N=4 64KiB x 4096 stripes (1 GiB user data), pairs cycle all 15"),
+    2: dict(p=13, N=12, nbytes=4 << 20, stripes=256, sparse=0, ops="enc+rec",
+            desc="c2: p=13 N=12 (12-bit words) 4MiB x 256 stripes, encode + recover, pairs cycle all 91"),
+    3: dict(p=257, N=64, nbytes=16 << 20, stripes=4, sparse=0, ops="enc",
+            desc="c3: p=257 N=64 (256-bit words) 16MiB x 4 stripes (4 GiB user data), encode only"),
+    4: dict(p=59, N=58, nbytes=8 << 20, stripes=64, sparse=2, ops="enc+dd",
+            desc="c4 wave: p=59 N=58 8MiB x 64 stripes (odd stripes sparse 0.9), encode + DD recovery"),
+    5: dict(p=61, N=60, nbytes=32 << 20, stripes=16, sparse=0, ops="rec",
+            desc="c5 wave: p=61 N=60 32MiB x 16 stripes, degraded-stream recovery (mixed classes)"),
+}
+METRIC = "encode and 2-erasure recover GB/s of user data per GPU and at 8 GPUs; % HBM roofline"
+
+
+def _env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def pair_schedule(cfg, N, stripes, stripe0, step):
+    """Erasure pair of each stripe for a given step (host list of (i, j))."""
+    import synthetic
+    allp = synthetic.all_pairs(N)
+    if cfg == 4:  # double-data-disk recovery: (s mod 1653)-th data pair
+        dd = [(i, j) for i in range(N) for j in range(i + 1, N)]
+        return [dd[(stripe0 + s) % len(dd)] for s in range(stripes)]
+    if cfg == 5:  # degraded stream: seeded class + indices per stripe
+        return [synthetic.erasure_pair(0, 5, stripe0 + s + step * stripes, N) for s in range(stripes)]
+    return [allp[(stripe0 + s + 37 * step) % len(allp)] for s in range(stripes)]
+
+
+def alg_bytes_recover(N, nbytes, pb, pairs):
+    """N surviving strips read + 2 rebuilt strips written = every strip of the stripe once."""
+    return len(pairs) * (N * nbytes + 2 * pb)
+
+
+def traffic_from_profile(cfg):
+    """dram bytes (read+write) per launch from the committed `ncu --set full` summary, or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"c{cfg}")
+    except Exception:
+        return None
+
+
+# ====================================================================== our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_cs_0611109_b200 import raid6c as R
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = CONFIGS[args.config]
+    p, N, nbytes, S = c["p"], c["N"], c["nbytes"], args.stripes or c["stripes"]
+    pb = R.parity_bytes(p, nbytes)
+    ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
+    stripe0 = rank * S  # weak scaling: each rank owns distinct global stripes
+    stream = torch.cuda.Stream(device=dev)
+    data = torch.empty((S, N, ss), dtype=torch.uint8, device=dev)
+    par = torch.zeros((S, 2, ps), dtype=torch.uint8, device=dev)
+    R.fill(data, ss, N * ss, nbytes, N, S, 0, args.config, stripe0, 0, c["sparse"], stream)
+    plan = R.Plan(p, N, nbytes, local, stream)
+    a_data, a_par = int(data.data_ptr()), int(par.data_ptr())
+    enc_args = (a_data, ss, N * ss, a_par, a_par + ps, 2 * ps, S)
+    ops = c["ops"]
+    do_enc = ops.startswith("enc")
+    do_rec = ops != "enc"
+    if not do_enc:  # recovery-only stream still needs valid parity: encode once (untimed)
+        plan.encode_strided(*enc_args)
+    total_steps = args.warmup + args.steps
+    pair_lists = [pair_schedule(args.config, N, S, stripe0, t) for t in range(total_steps)]
+    pair_dev = [torch.tensor(pl, dtype=torch.int32, device=dev) for pl in pair_lists]
+    torch.cuda.synchronize(dev)
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(total_steps)]
+
+    def step(t):
+        with torch.cuda.stream(stream):
+            ev[t][0].record(stream)
+            if do_enc:
+                plan.encode_strided(*enc_args)
+            ev[t][1].record(stream)
+            if do_rec:
+                plan.recover_strided(*enc_args, pair_dev[t])
+            ev[t][2].record(stream)
+
+    for t in range(args.warmup):
+        step(t)
+    stream.synchronize()
+    # snapshot for verification after the timed region (recovery rewrites lost strips in place)
+    ref_data, ref_par = (data.clone(), par.clone()) if args.verify else (None, None)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = R.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for t in range(args.warmup, total_steps):
+        step(t)
+    t_end.record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize(dev)
+    launches = R.launch_count() - launches0
+    clk = clocks.stop()
+    plan.sync()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    enc_ms = [ev[t][0].elapsed_time(ev[t][1]) for t in range(args.warmup, total_steps)]
+    rec_ms = [ev[t][1].elapsed_time(ev[t][2]) for t in range(args.warmup, total_steps)]
+    if world > 1:
+        tt = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(tt.item())
+
+    # ---------------------------------------------------------------- verification
+    verified = None
+    if args.verify:
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        if do_rec:
+            # ref snapshot was taken after warm-up steps; data/parity must be bit-identical
+            R.count_mismatch(data, ref_data, data.numel(), cnt, stream)
+            R.count_mismatch(par, ref_par, par.numel(), cnt, stream)
+        stream.synchronize()
+        mism = int(cnt.item())
+        checked = 2 * data.numel() if do_rec else 0
+        oracle_ok = None
+        if rank == 0 and args.oracle_check:
+            oracle_ok = oracle_sample_check(p, N, nbytes, args.config, c["sparse"], stripe0, par)
+        tot = torch.tensor([mism, checked], dtype=torch.int64, device=dev)
+        if world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        verified = {"mismatched_bytes": int(tot[0].item()), "checked_bytes": int(tot[1].item()),
+                    "oracle_segments_match": oracle_ok}
+        del ref_data, ref_par
+
+    # ---------------------------------------------------------------- e2e (host buffers, public API)
+    e2e = None
+    if args.e2e and do_enc:
+        e2e = run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_lists, do_rec, world, dev)
+
+    user_bytes_step = (int(do_enc) + int(do_rec)) * N * nbytes * S
+    value = world * user_bytes_step * args.steps / (elapsed_ms / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    enc_alg = S * (N * nbytes + 2 * pb)
+    rec_alg = alg_bytes_recover(N, nbytes, pb, pair_lists[-1]) if do_rec else 0
+    kern = []
+    if do_enc:
+        d = statistics.mean(enc_ms)
+        kern.append(("encode", enc_alg, d))
+    if do_rec:
+        d = statistics.mean(rec_ms)
+        kern.append(("recover", rec_alg, d))
+    dom = max(kern, key=lambda k: k[2])
+    traffic = traffic_from_profile(args.config)
+    roof = {
+        "kernel": f"zp_kernel<{p},{'true' if dom[0] == 'recover' else 'false'}> ({dom[0]})",
+        "bound": "hbm", "achieved": round(dom[1] / (dom[2] / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
+        "frac": round(dom[1] / (dom[2] / 1e3) / 1e9 / peak, 4), "peak_source": peak_src,
+        "traffic": traffic.get(dom[0]) if isinstance(traffic, dict) else None,
+        "alg_bytes_per_launch": dom[1], "avg_launch_ms": round(dom[2], 4),
+    }
+    per_kernel = {k[0]: {"alg_bytes": k[1], "avg_ms": round(k[2], 4),
+                         "achieved_GBps": round(k[1] / (k[2] / 1e3) / 1e9, 1),
+                         "frac_of_peak": round(k[1] / (k[2] / 1e3) / 1e9 / peak, 4),
+                         "frac_of_8TBps": round(k[1] / (k[2] / 1e3) / 1e9 / 8000.0, 4),
+                         "user_GBps": round(S * N * nbytes / (k[2] / 1e3) / 1e9, 1)} for k in kern}
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(elapsed_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 (bitwise GF(2) words)",
+        "data": "synthetic (seeded SplitMix64 counter generator, generated on device)",
+        "config": {"workload": c["desc"], "p": p, "N": N, "strip_bytes": nbytes, "parity_bytes": pb,
+                   "stripes_per_gpu": S, "ops": ops, "parallelism": f"stripe-sharded x{world} (no data-path collective)",
+                   "l2": "working set >= 1 GiB >> 126 MB L2 (no flush needed)"},
+        "roofline": roof, "kernels": per_kernel, "gpu_launches": launches, "clocks": clk,
+        "verified": verified, "e2e": e2e,
+        "fast_path": R.has_fast_path(p),
+    }
+    if rank == 0 and args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, p, N, nbytes, args.config, c["sparse"])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_lists, do_rec, world, dev):
+    """Same workload through the host-buffer public API (raid6c_encode_host/recover_host):
+    H2D of inputs and D2H of results inside the timed region, pinned host memory."""
+    hd = torch.empty((S, N, ss), dtype=torch.uint8).pin_memory()
+    hp = torch.zeros((S, 2, ps), dtype=torch.uint8).pin_memory()
+    hd.copy_(data.cpu())
+    hd_ptr, hp_ptr = int(hd.data_ptr()), int(hp.data_ptr())
+    a = (hd_ptr, ss, N * ss, hp_ptr, hp_ptr + ps, 2 * ps, S)
+    steps = max(1, args.e2e_steps)
+    times, h2d, d2h = [], 0, 0
+    for t in range(1 + steps):
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        t0 = time.perf_counter()
+        plan.encode_host(*a)
+        b1 = plan.host_traffic()
+        if do_rec:
+            plan.recover_host(*a, pair_lists[t % len(pair_lists)])
+            b2 = plan.host_traffic()
+        else:
+            b2 = (0, 0)
+        t1 = time.perf_counter()
+        if t >= 1:
+            times.append(t1 - t0)
+            h2d, d2h = b1[0] + b2[0], b1[1] + b2[1]
+    # correctness of the host path vs the device path (parity of the same stripes)
+    same = bool(torch.equal(hp[:, :, :pb], par[:, :, :pb].cpu()))
+    tm = statistics.mean(times)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([tm], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tm = float(tt.item())
+    user = (1 + int(do_rec)) * N * nbytes * S * world
+    return {"value": round(user / tm / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "steps": steps, "s_per_step": round(tm, 4),
+            "api": "raid6c_encode_host + raid6c_recover_host (pinned host buffers)",
+            "matches_device_path": same}
+
+
+def oracle_sample_check(p, N, nbytes, cfg, sparse_mode, stripe0, par):
+    """Sampled word-aligned P/Q segments of two stripes against the CPU oracle."""
+    import numpy as np
+    import oracle
+    import synthetic
+    n = p - 1
+    ok = True
+    for s in (0, par.shape[0] - 1):
+        gs = stripe0 + s
+        sparse = sparse_mode == 1 or (sparse_mode == 2 and gs % 2 == 1)
+        W = (8 * nbytes + n - 1) // n
+        for g0 in (0, (W // 8) // 2, max(0, W // 8 - 2)):
+            b0 = g0 * n
+            b1 = min(nbytes, b0 + 2 * n)
+            if g0 == max(0, W // 8 - 2):
+                b1 = nbytes
+            segs = [synthetic.strip_bytes(0, cfg, gs, k, nbytes, sparse, lo=b0, hi=b1) for k in range(N)]
+            P, Q = oracle.encode(p, segs, b1 - b0)
+            e = b0 + P.size
+            ok &= bool(np.array_equal(par[s, 0, b0:e].cpu().numpy(), P))
+            ok &= bool(np.array_equal(par[s, 1, b0:e].cpu().numpy(), Q))
+    return ok
+
+
+# ====================================================================== oracle (CPU) arm
+def _oracle_work(p, N, nbytes, cfg, sparse_mode, budget_s, max_threads):
+    """Time the oracle as it stands on a bounded sample of the same workload: per stripe,
+    encode + one recovery (pair from the same schedule).  Returns (user_bytes, seconds, threads, sample)."""
+    import concurrent.futures as cf
+    import numpy as np
+    import oracle
+    import synthetic
+    oracle.build()
+    ncores = len(os.sched_getaffinity(0))
+    threads = max(1, min(ncores, max_threads))
+    ops = CONFIGS[cfg]["ops"]
+    # bounded strip length so one task is ~1-3 s of CPU work
+    sample_bytes = min(nbytes, 1 << 20)
+    pb = oracle.parity_bytes(p, sample_bytes)
+
+    def task(s):
+        sparse = sparse_mode == 1 or (sparse_mode == 2 and s % 2 == 1)
+        data = [synthetic.strip_bytes(0, cfg, s, k, nbytes, sparse, lo=0, hi=sample_bytes) for k in range(N)]
+        t0 = time.perf_counter()
+        user = 0
+        P, Q = oracle.encode(p, data, sample_bytes)
+        if ops != "rec":
+            user += N * sample_bytes
+        if ops != "enc":
+            i, j = pair_schedule(cfg, N, 1, s, 0)[0]
+            strips = [d.copy() for d in data] + [P.copy(), Q.copy()]
+            strips[i][:] = 0
+            strips[j][:] = 0
+            oracle.recover(p, N, i, j, strips, sample_bytes)
+            user += N * sample_bytes
+        return user, time.perf_counter() - t0
+
+    # calibrate one task, then size the sample to the budget
+    u0, t0 = task(0)
+    per = max(t0, 1e-3)
+    ntasks = max(threads, int(budget_s * threads / per))
+    ntasks = min(ntasks, 4 * threads)
+    t_start = time.perf_counter()
+    users = 0
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        for u, _ in ex.map(task, range(1, 1 + ntasks)):
+            users += u
+    wall = time.perf_counter() - t_start
+    sample = (f"{ntasks} stripes x {N} strips truncated to {sample_bytes} B "
+              f"({'encode' if ops != 'rec' else ''}{' + ' if ops == 'enc+rec' or ops == 'enc+dd' else ''}"
+              f"{'one recovery' if ops != 'enc' else ''} each), bit-array oracle, {threads} threads")
+    return users, wall, threads, sample
+
+
+def cpu_baseline(args, p, N, nbytes, cfg, sparse_mode):
+    users, wall, threads, sample = _oracle_work(p, N, nbytes, cfg, sparse_mode, args.cpu_budget, args.cpu_threads)
+    return {"value": round(users / wall / 1e9, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
+            "sample": sample, "seconds": round(wall, 2)}
+
+
+def run_reference(args):
+    rank, world, _ = _env_rank()
+    if rank != 0:
+        return  # under torchrun only rank 0 runs the CPU arm
+    c = CONFIGS[args.config]
+    p, N, nbytes = c["p"], c["N"], c["nbytes"]
+    vals, cores, sample, secs = [], 0, "", []
+    budget = max(2.0, args.cpu_budget / max(1, args.steps + args.warmup))
+    for t in range(args.warmup + args.steps):
+        users, wall, threads, sample = _oracle_work(p, N, nbytes, args.config, c["sparse"], budget, args.cpu_threads)
+        if t >= args.warmup:
+            vals.append(users / wall / 1e9)
+            secs.append(wall)
+        cores = threads
+    v = statistics.mean(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.mean(secs), 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bit arrays (uint8 per bit)",
+        "data": "synthetic (seeded SplitMix64 counter generator)",
+        "config": {"workload": c["desc"], "p": p, "N": N, "strip_bytes": nbytes, "ops": c["ops"]},
+        "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--stripes", type=int, default=0, help="override stripes per GPU per step")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-verify", dest="verify", action="store_false")
+    ap.add_argument("--no-oracle-check", dest="oracle_check", action="store_false")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--cpu-threads", type=int, default=64)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warm-up raised to 3 (timing rule)", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

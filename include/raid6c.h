@@ -1,0 +1,186 @@
+/*
+ * raid6c.h -- C ABI of the B200-native Z_p-RAID library (libraid6c.so).
+ *
+ * Method: "An approach to RAID-6 based on cyclic groups" (arxiv cs/0611109).  A stripe is
+ * N data strips d_0..d_{N-1} plus two parity strips P and Q.  Each strip is an LSB-first
+ * bit stream of (p-1)-bit words, word w = stream bits [w(p-1), (w+1)(p-1)), bit j of a word
+ * = coefficient of x^j of an element of R_p = F2[x]/(1 + x + ... + x^{p-1})
+ * (Sec. 4.5; readings R1, R2).
+ *
+ *   P = d_0 + d_1 + ... + d_{N-1},   Q = d_0 + x d_1 + ... + x^{N-1} d_{N-1}
+ *       (Eq. (znparity), Corollary 24.4; 0-based as Eq. (rsparity),
+ *        PAPER.md:831-834; multiplication by x is the Sylvester matrix)
+ *
+ * and any two lost strips are rebuilt from the other N (Lemma 23.2, PAPER.md:370-406;
+ * Sec. 4.3/4.6).
+ *
+ * Conventions for every call:
+ *   - Strip indices: 0..N-1 data, N = P, N+1 = Q (R4).
+ *   - Data strips are `bytes` long.  P and Q are raid6c_parity_bytes(p, bytes) long: the
+ *     data are zero-extended to W = ceil(8*bytes/(p-1)) whole words and the parity holds all
+ *     W*(p-1) bits; parity bits past W*(p-1) are written as zero (R5).
+ *   - p is an odd prime, 3 <= p <= 257; 1 <= N <= p (R6, R7).
+ *   - Pointers named "device" must be CUDA device memory of the plan's device; the caller
+ *     owns all strip memory (the library never allocates or frees it).  A plan owns only
+ *     small device/pinned work buffers, freed by raid6c_plan_destroy.
+ *   - Lost strips are outputs: their input contents are never read.  All other strips are
+ *     read-only inputs.  A recovered data strip is written for exactly `bytes` bytes.
+ *   - Argument errors are returned synchronously, before any launch, with no side effect.
+ *     Device-side failures are sticky and reported by raid6c_sync (and by the synchronous
+ *     convenience calls).  There is no CPU fallback: every byte is computed by the
+ *     library's sm_100a kernels.
+ *   - Plan calls are stream-ordered on the plan's stream and return before completion.
+ *     A plan is not thread-safe; distinct plans are independent.
+ *   - Any alignment is accepted.  The TMA fast path needs every strip base and stride
+ *     16-byte aligned; otherwise the (slower) direct-load path of the same kernel runs.
+ */
+#ifndef RAID6C_H
+#define RAID6C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define RAID6C_MAX_P 257
+#define RAID6C_MAX_STRIPS (RAID6C_MAX_P + 2)
+
+typedef enum {
+    RAID6C_OK = 0,
+    RAID6C_E_INVALID_P = 1,     /* p is not an odd prime in [3, 257] */
+    RAID6C_E_INVALID_N = 2,     /* N < 1 or N > p */
+    RAID6C_E_INVALID_INDEX = 3, /* lost index outside [0, N+2) or lost_i == lost_j */
+    RAID6C_E_NULL = 4,          /* a required pointer is NULL */
+    RAID6C_E_SIZE = 5,          /* bytes == 0, num_stripes < 0, or a stride smaller than its strip */
+    RAID6C_E_CUDA = 6,          /* CUDA runtime / launch error (sticky; see raid6c_last_cuda_error) */
+    RAID6C_E_NO_DEVICE = 7,     /* no CUDA device, or the device is not sm_100 */
+    RAID6C_E_PLAN = 8           /* plan/call mismatch (p, N or bytes differ from the plan) */
+} raid6c_status;
+
+/* One erasure pair per stripe for batched recovery (either order; -1 is not allowed). */
+typedef struct {
+    int32_t lost_i;
+    int32_t lost_j;
+} raid6c_erasure;
+
+typedef struct raid6c_plan_s *raid6c_plan;
+
+/* ---------------------------------------------------------------- sizes (host only) */
+
+/* W = ceil(8*bytes/(p-1)), the number of ring words per strip (R5).
+ * Returns 0 for an invalid p. */
+size_t raid6c_word_count(int p, size_t bytes);
+
+/* Parity strip length ceil(W*(p-1)/8) bytes (R5).  0 for an invalid p. */
+size_t raid6c_parity_bytes(int p, size_t bytes);
+
+/* 1 if p is accepted (odd prime in [3,257]), else 0. */
+int raid6c_valid_p(int p);
+
+/* 1 if p has a specialised (compile-time-p) TMA kernel, 0 if it runs the generic kernel. */
+int raid6c_has_fast_path(int p);
+
+/* Static description of the status code (never NULL). */
+const char *raid6c_status_string(raid6c_status s);
+
+/* Text of the last CUDA error seen by this thread (empty string if none). */
+const char *raid6c_last_cuda_error(void);
+
+/* Number of kernels this process has launched through the library (all plans). */
+uint64_t raid6c_launch_count(void);
+
+/* ---------------------------------------------------------------- plans */
+
+/* Create a plan for (p, N, bytes) on CUDA device `device`, ordering work on `stream`
+ * (a cudaStream_t; NULL = the legacy default stream).  The plan validates p and N once,
+ * selects the kernel (fast or generic) and owns its small work buffers. */
+raid6c_status raid6c_plan_create(raid6c_plan *out, int p, int N, size_t bytes, int device, void *stream);
+raid6c_status raid6c_plan_destroy(raid6c_plan plan);
+raid6c_status raid6c_plan_set_stream(raid6c_plan plan, void *stream);
+
+/* Wait for all work of the plan's stream; returns the first sticky error (and clears it). */
+raid6c_status raid6c_sync(raid6c_plan plan);
+
+/* ------------------------------------------- north-star single-stripe calls (synchronous) */
+
+/* Encode one stripe on the current CUDA device (Eq. (znparity)).
+ * strips: HOST array of N DEVICE pointers (data strips, `bytes` each);  P, Q: DEVICE
+ * pointers of raid6c_parity_bytes(p, bytes).  Synchronous: returns after the kernel has
+ * completed, with its status. */
+raid6c_status raid6c_encode(int p, int N, const uint8_t *const *strips, uint8_t *P, uint8_t *Q, size_t bytes);
+
+/* Rebuild lost strips lost_i and lost_j (any order) of one stripe (Lemma 23.2,
+ * PAPER.md:370-406; Sec. 4.6).  strips: HOST array of N+2 DEVICE
+ * pointers, 0..N-1 data (`bytes`), N = P, N+1 = Q (parity_bytes).  The two lost strips are
+ * written, the rest read.  Synchronous. */
+raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t *const *strips, size_t bytes);
+
+/* ------------------------------------------------ batched, stream-ordered device calls */
+
+/* Encode num_stripes stripes.  Data strip k of stripe s is at
+ *   data + s*stripe_stride + k*strip_stride            (DEVICE, `bytes` long)
+ * and its parity at  P + s*parity_stride,  Q + s*parity_stride  (DEVICE, parity_bytes).
+ * Requires strip_stride >= bytes, stripe_stride >= N*strip_stride (or num_stripes == 1),
+ * parity_stride >= parity_bytes unless num_stripes == 1. */
+raid6c_status raid6c_encode_strided(raid6c_plan plan, const uint8_t *data, size_t strip_stride,
+                                    size_t stripe_stride, uint8_t *P, uint8_t *Q,
+                                    size_t parity_stride, int num_stripes);
+
+/* Recover num_stripes stripes in place (same layout as raid6c_encode_strided): for stripe s
+ * the strips named by erasures[s] (or erasures[0] for every stripe when num_erasures == 1)
+ * are rebuilt from the other N strips of that stripe.  `erasures` is a HOST array when
+ * erasures_on_device == 0, else a DEVICE array (already validated by the caller: each pair
+ * distinct and in [0, N+2)).  Stripes may mix erasure classes (DD, DP, DQ, PQ). */
+raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t *data, size_t strip_stride,
+                                     size_t stripe_stride, uint8_t *P, uint8_t *Q,
+                                     size_t parity_stride, int num_stripes,
+                                     const raid6c_erasure *erasures, int num_erasures,
+                                     int erasures_on_device);
+
+/* ------------------------------------------------ host-buffer calls (end-to-end path) */
+
+/* Same as the strided calls, but every pointer is HOST memory (pinned memory gives
+ * full-duplex PCIe overlap; pageable memory works but is slower).  The plan streams the
+ * stripes through its own device staging ring: H2D copy, kernel and D2H copy of
+ * successive chunks overlap on separate streams.  Synchronous: returns when the results
+ * are in host memory.  For recovery only the surviving strips are copied in and only
+ * the two rebuilt strips of each stripe are copied out. */
+raid6c_status raid6c_encode_host(raid6c_plan plan, const uint8_t *data, size_t strip_stride,
+                                 size_t stripe_stride, uint8_t *P, uint8_t *Q,
+                                 size_t parity_stride, int num_stripes);
+raid6c_status raid6c_recover_host(raid6c_plan plan, uint8_t *data, size_t strip_stride,
+                                  size_t stripe_stride, uint8_t *P, uint8_t *Q,
+                                  size_t parity_stride, int num_stripes,
+                                  const raid6c_erasure *erasures, int num_erasures);
+
+/* Bytes moved host->device and device->host by the last *_host call on this plan. */
+raid6c_status raid6c_host_traffic(raid6c_plan plan, uint64_t *h2d_bytes, uint64_t *d2h_bytes);
+
+/* ------------------------------------------------ harness kernels (not the method) */
+
+/* Fill DEVICE strips with the synthetic generator of synthetic/gen.py (DESIGN.md "input
+ * recipe"): for s in [0, nstripes), t in [0, nstrips) the `len` bytes at
+ * dst + s*stripe_stride + t*strip_stride get strip (strip0 + t) of stripe (stripe0 + s) of
+ * config `cfg`.  sparse_mode: 0 uniform, 1 sparse (each byte 0 with probability 0.9),
+ * 2 sparse for odd global stripe indices only (config 4).  Stream-ordered on `stream`. */
+raid6c_status raid6c_fill(uint8_t *dst, size_t strip_stride, size_t stripe_stride, size_t len, int nstrips,
+                          int nstripes, uint64_t seed, int cfg, int stripe0, int strip0, int sparse_mode,
+                          void *stream);
+
+/* Count mismatching bytes between two DEVICE buffers; the count is added to *count_dev
+ * (a DEVICE uint64).  Stream-ordered. */
+raid6c_status raid6c_count_mismatch(const uint8_t *a, const uint8_t *b, size_t len,
+                                    uint64_t *count_dev, void *stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* RAID6C_H */

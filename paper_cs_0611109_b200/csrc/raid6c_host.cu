@@ -1,0 +1,687 @@
+// raid6c_host.cu -- host side of libraid6c: argument validation, plans, kernel selection and
+// launch, the host-buffer streaming pipeline, and the C ABI entry points of include/raid6c.h.
+// Every byte of the method is computed by the sm_100a kernels (zp_fast.cuh / zp_generic.cu);
+// there is no CPU fallback anywhere in this file.
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "raid6c.h"
+#include "zp_args.h"
+
+namespace zp {
+// fast-path instantiations (zp_fast_p*.cu)
+const FastEntry* fast_entry_3();
+const FastEntry* fast_entry_5();
+const FastEntry* fast_entry_7();
+const FastEntry* fast_entry_13();
+const FastEntry* fast_entry_17();
+const FastEntry* fast_entry_59();
+const FastEntry* fast_entry_61();
+const FastEntry* fast_entry_257();
+
+const FastEntry* fast_entry(int p) {
+  switch (p) {
+    case 3: return fast_entry_3();
+    case 5: return fast_entry_5();
+    case 7: return fast_entry_7();
+    case 13: return fast_entry_13();
+    case 17: return fast_entry_17();
+    case 59: return fast_entry_59();
+    case 61: return fast_entry_61();
+    case 257: return fast_entry_257();
+    default: return nullptr;
+  }
+}
+
+cudaError_t harness_fill(uint8_t* dst, uint64_t strip_stride, uint64_t stripe_stride, uint64_t len, int nstrips,
+                         int nstripes, uint64_t seed, int cfg, int stripe0, int strip0, int sparse_mode,
+                         cudaStream_t st);
+cudaError_t harness_count_mismatch(const uint8_t* a, const uint8_t* b, uint64_t len, uint64_t* out, cudaStream_t st);
+}  // namespace zp
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+thread_local std::string g_last_err;
+
+raid6c_status cuda_fail(cudaError_t e) {
+  g_last_err = cudaGetErrorString(e);
+  return RAID6C_E_CUDA;
+}
+#define ZP_CUDA(call)                              \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return cuda_fail(e_);   \
+  } while (0)
+
+bool is_valid_p(int p) {
+  if (p < 3 || p > RAID6C_MAX_P || (p % 2) == 0) return false;
+  for (int d = 3; d * d <= p; d += 2)
+    if (p % d == 0) return false;
+  return true;
+}
+
+size_t word_count(int p, size_t bytes) { return (8 * bytes + (p - 2)) / (p - 1); }
+size_t parity_bytes(int p, size_t bytes) { return (word_count(p, bytes) * (p - 1) + 7) / 8; }
+
+// per-(device, kernel) one-time attribute setup
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, int> g_occ;  // -> CTAs per SM
+
+raid6c_status kernel_occupancy(int device, const void* fn, int threads, size_t smem, int* occ) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto key = std::make_pair(device, fn);
+  auto it = g_occ.find(key);
+  if (it != g_occ.end()) {
+    *occ = it->second;
+    return RAID6C_OK;
+  }
+  ZP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  int o = 0;
+  ZP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem));
+  if (o < 1) o = 1;
+  g_occ[key] = o;
+  *occ = o;
+  return RAID6C_OK;
+}
+
+}  // namespace
+
+struct raid6c_plan_s {
+  int p = 0, N = 0;
+  size_t bytes = 0, pbytes = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  const zp::FastEntry* fe = nullptr;
+  int num_sms = 148;
+  int occ_enc = 1, occ_rec = 1;
+  int2* d_er = nullptr;
+  size_t er_cap = 0;
+  raid6c_status sticky = RAID6C_OK;
+  // host-buffer pipeline
+  uint8_t* d_stage = nullptr;
+  size_t slot_bytes = 0;
+  int slot_stripes = 0;
+  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // in, kernel, out
+  cudaEvent_t ev_in[2] = {}, ev_k[2] = {}, ev_out[2] = {};
+  bool host_ready = false;
+  uint64_t h2d = 0, d2h = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, cudaStream_t stream) {
+  if (!is_valid_p(p)) return RAID6C_E_INVALID_P;
+  if (N < 1 || N > p) return RAID6C_E_INVALID_N;
+  if (bytes == 0) return RAID6C_E_SIZE;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0 || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    g_last_err = "no CUDA device";
+    return RAID6C_E_NO_DEVICE;
+  }
+  cudaDeviceProp prop;
+  ZP_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) {
+    g_last_err = "libraid6c is built for sm_100a only";
+    return RAID6C_E_NO_DEVICE;
+  }
+  pl->p = p;
+  pl->N = N;
+  pl->bytes = bytes;
+  pl->pbytes = parity_bytes(p, bytes);
+  pl->device = device;
+  pl->stream = stream;
+  pl->num_sms = prop.multiProcessorCount;
+  pl->fe = zp::fast_entry(p);
+  if (pl->fe) {
+    DeviceGuard g(device);
+    raid6c_status st = kernel_occupancy(device, pl->fe->enc_kernel, pl->fe->threads + 32, pl->fe->smem_bytes, &pl->occ_enc);
+    if (st != RAID6C_OK) return st;
+    st = kernel_occupancy(device, pl->fe->rec_kernel, pl->fe->threads + 32, pl->fe->smem_bytes, &pl->occ_rec);
+    if (st != RAID6C_OK) return st;
+  }
+  return RAID6C_OK;
+}
+
+void plan_release(raid6c_plan pl) {
+  DeviceGuard g(pl->device);
+  if (pl->d_er) cudaFree(pl->d_er);
+  if (pl->d_stage) cudaFree(pl->d_stage);
+  for (int i = 0; i < 3; i++)
+    if (pl->hs[i]) cudaStreamDestroy(pl->hs[i]);
+  for (int i = 0; i < 2; i++) {
+    if (pl->ev_in[i]) cudaEventDestroy(pl->ev_in[i]);
+    if (pl->ev_k[i]) cudaEventDestroy(pl->ev_k[i]);
+    if (pl->ev_out[i]) cudaEventDestroy(pl->ev_out[i]);
+  }
+}
+
+// Launch one batch (all stripes share p, N, bytes).  a.base / strides / erasures are set.
+raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, bool recover, cudaStream_t st) {
+  if (a.num_stripes == 0) return RAID6C_OK;
+  a.N = pl->N;
+  a.bytes = pl->bytes;
+  a.pbytes = pl->pbytes;
+  cudaError_t err;
+  if (pl->fe) {
+    const zp::FastEntry* fe = pl->fe;
+    bool aligned = true;
+    for (int k = 0; k < pl->N + 2; k++) aligned &= (reinterpret_cast<uintptr_t>(a.base[k]) & 15u) == 0;
+    if (a.num_stripes > 1) aligned &= (a.data_stride % 16 == 0) && (a.parity_stride % 16 == 0);
+    const uint64_t TB = static_cast<uint64_t>(fe->tile_bytes), CB = static_cast<uint64_t>(fe->chunk_bytes);
+    a.body_tiles = aligned ? pl->bytes / TB : 0;
+    const uint64_t body_end = a.body_tiles * TB;
+    a.tail_units_per_stripe = (pl->pbytes - body_end + CB - 1) / CB;
+    const uint64_t items = a.body_tiles * static_cast<uint64_t>(a.num_stripes);
+    const uint64_t tail_ctas =
+        (a.tail_units_per_stripe * static_cast<uint64_t>(a.num_stripes) + fe->threads - 1) / fe->threads;
+    const uint64_t cap = static_cast<uint64_t>(pl->num_sms) * (recover ? pl->occ_rec : pl->occ_enc);
+    uint64_t grid = std::min<uint64_t>(cap, std::max<uint64_t>(items, tail_ctas));
+    if (grid == 0) grid = 1;
+    void* args[] = {&a};
+    err = cudaLaunchKernel(recover ? fe->rec_kernel : fe->enc_kernel, dim3(static_cast<unsigned>(grid)),
+                           dim3(fe->threads + 32), args, fe->smem_bytes, st);
+  } else {
+    err = zp::generic_launch(a, pl->p, recover, st, pl->num_sms);
+  }
+  if (err != cudaSuccess) {
+    pl->sticky = RAID6C_E_CUDA;
+    return cuda_fail(err);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return RAID6C_OK;
+}
+
+raid6c_status check_erasure(int N, int i, int j) {
+  if (i == j || i < 0 || j < 0 || i >= N + 2 || j >= N + 2) return RAID6C_E_INVALID_INDEX;
+  return RAID6C_OK;
+}
+
+raid6c_status strided_args(raid6c_plan pl, const uint8_t* data, size_t strip_stride, size_t stripe_stride,
+                           const uint8_t* P, const uint8_t* Q, size_t parity_stride, int num_stripes,
+                           zp::ZpArgs& a) {
+  if (!pl) return RAID6C_E_NULL;
+  if (num_stripes < 0) return RAID6C_E_SIZE;
+  if (!data || !P || !Q) return RAID6C_E_NULL;
+  if (pl->N > 1 && strip_stride < pl->bytes) return RAID6C_E_SIZE;
+  if (num_stripes > 1 && (stripe_stride < pl->bytes || parity_stride < pl->pbytes)) return RAID6C_E_SIZE;
+  std::memset(&a, 0, sizeof(a));
+  for (int k = 0; k < pl->N; k++) a.base[k] = data + static_cast<size_t>(k) * strip_stride;
+  a.base[pl->N] = P;
+  a.base[pl->N + 1] = Q;
+  a.data_stride = stripe_stride;
+  a.parity_stride = parity_stride;
+  a.num_stripes = num_stripes;
+  a.ei = pl->N;
+  a.ej = pl->N + 1;
+  return RAID6C_OK;
+}
+
+// Upload host erasure pairs (validated, canonical) into the plan's device buffer.
+raid6c_status upload_erasures(raid6c_plan pl, const raid6c_erasure* er, int count, cudaStream_t st) {
+  std::vector<int2> h(count);
+  for (int s = 0; s < count; s++) {
+    const int i = er[s].lost_i, j = er[s].lost_j;
+    raid6c_status e = check_erasure(pl->N, i, j);
+    if (e != RAID6C_OK) return e;
+    h[s] = make_int2(std::min(i, j), std::max(i, j));
+  }
+  if (static_cast<size_t>(count) > pl->er_cap) {
+    DeviceGuard g(pl->device);
+    if (pl->d_er) {
+      ZP_CUDA(cudaStreamSynchronize(st));
+      cudaFree(pl->d_er);
+      pl->d_er = nullptr;
+    }
+    size_t cap = std::max<size_t>(1024, static_cast<size_t>(count));
+    ZP_CUDA(cudaMalloc(&pl->d_er, cap * sizeof(int2)));
+    pl->er_cap = cap;
+  }
+  // pageable source: the copy is staged before this call returns, so `h` may be freed
+  ZP_CUDA(cudaMemcpyAsync(pl->d_er, h.data(), count * sizeof(int2), cudaMemcpyHostToDevice, st));
+  return RAID6C_OK;
+}
+
+// ------------------------------------------------------------------ cached single-stripe plans
+std::mutex g_cache_mu;
+std::map<std::tuple<int, int, int, size_t>, raid6c_plan> g_cache;
+
+raid6c_status cached_plan(int p, int N, size_t bytes, raid6c_plan* out) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    g_last_err = "no CUDA device";
+    return RAID6C_E_NO_DEVICE;
+  }
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto key = std::make_tuple(dev, p, N, bytes);
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) {
+    *out = it->second;
+    return RAID6C_OK;
+  }
+  raid6c_plan pl = new raid6c_plan_s();
+  raid6c_status st = plan_init(pl, p, N, bytes, dev, nullptr);
+  if (st != RAID6C_OK) {
+    delete pl;
+    return st;
+  }
+  if (g_cache.size() > 64) {  // bounded cache
+    for (auto& kv : g_cache) {
+      plan_release(kv.second);
+      delete kv.second;
+    }
+    g_cache.clear();
+  }
+  g_cache[key] = pl;
+  *out = pl;
+  return RAID6C_OK;
+}
+
+// ------------------------------------------------------------------ host-buffer pipeline
+raid6c_status host_setup(raid6c_plan pl, int num_stripes) {
+  DeviceGuard g(pl->device);
+  const size_t sd = (pl->bytes + 255) / 256 * 256, sp = (pl->pbytes + 255) / 256 * 256;
+  const size_t stripe_dev = static_cast<size_t>(pl->N) * sd + 2 * sp;
+  const size_t target = size_t(512) << 20;
+  int cs = static_cast<int>(std::max<size_t>(1, target / stripe_dev));
+  cs = std::min(cs, std::max(1, num_stripes));
+  const size_t need = static_cast<size_t>(cs) * stripe_dev;
+  if (!pl->host_ready) {
+    for (int i = 0; i < 3; i++) ZP_CUDA(cudaStreamCreateWithFlags(&pl->hs[i], cudaStreamNonBlocking));
+    for (int i = 0; i < 2; i++) {
+      ZP_CUDA(cudaEventCreateWithFlags(&pl->ev_in[i], cudaEventDisableTiming));
+      ZP_CUDA(cudaEventCreateWithFlags(&pl->ev_k[i], cudaEventDisableTiming));
+      ZP_CUDA(cudaEventCreateWithFlags(&pl->ev_out[i], cudaEventDisableTiming));
+    }
+    pl->host_ready = true;
+  }
+  if (pl->slot_bytes < need || pl->slot_stripes < cs) {
+    if (pl->d_stage) {
+      ZP_CUDA(cudaDeviceSynchronize());
+      cudaFree(pl->d_stage);
+      pl->d_stage = nullptr;
+    }
+    ZP_CUDA(cudaMalloc(&pl->d_stage, 2 * need));
+    pl->slot_bytes = need;
+    pl->slot_stripes = cs;
+  }
+  return RAID6C_OK;
+}
+
+// Copy `rows` strips of `width` bytes: host rows at src + r*spitch -> device rows at dst + r*dpitch.
+raid6c_status copy_rows(uint8_t* dst, size_t dpitch, const uint8_t* src, size_t spitch, size_t width, int rows,
+                        cudaMemcpyKind kind, cudaStream_t st) {
+  if (rows <= 0) return RAID6C_OK;
+  if (rows == 1) {
+    ZP_CUDA(cudaMemcpyAsync(dst, src, width, kind, st));
+  } else {
+    ZP_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, st));
+  }
+  return RAID6C_OK;
+}
+
+raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_t stripe_stride, uint8_t* P,
+                       uint8_t* Q, size_t parity_stride, int num_stripes, const raid6c_erasure* er,
+                       int num_erasures, bool recover) {
+  if (!pl) return RAID6C_E_NULL;
+  if (num_stripes < 0) return RAID6C_E_SIZE;
+  if (num_stripes == 0) return RAID6C_OK;
+  if (!data || !P || !Q) return RAID6C_E_NULL;
+  if (pl->N > 1 && strip_stride < pl->bytes) return RAID6C_E_SIZE;
+  if (num_stripes > 1 && (stripe_stride < pl->bytes || parity_stride < pl->pbytes)) return RAID6C_E_SIZE;
+  std::vector<int2> pairs;
+  if (recover) {
+    if (!er) return RAID6C_E_NULL;
+    if (num_erasures != 1 && num_erasures != num_stripes) return RAID6C_E_SIZE;
+    pairs.resize(num_stripes);
+    for (int s = 0; s < num_stripes; s++) {
+      const raid6c_erasure& e = er[num_erasures == 1 ? 0 : s];
+      raid6c_status c = check_erasure(pl->N, e.lost_i, e.lost_j);
+      if (c != RAID6C_OK) return c;
+      pairs[s] = make_int2(std::min(e.lost_i, e.lost_j), std::max(e.lost_i, e.lost_j));
+    }
+  }
+  raid6c_status st = host_setup(pl, num_stripes);
+  if (st != RAID6C_OK) return st;
+  DeviceGuard g(pl->device);
+  const int N = pl->N;
+  const size_t sd = (pl->bytes + 255) / 256 * 256, sp = (pl->pbytes + 255) / 256 * 256;
+  const int cs = pl->slot_stripes;
+  cudaStream_t s_in = pl->hs[0], s_k = pl->hs[1], s_out = pl->hs[2];
+  if (recover) {
+    // per-stripe pairs for the whole call, uploaded once on the kernel stream
+    std::vector<raid6c_erasure> ev(num_stripes);
+    for (int s = 0; s < num_stripes; s++) ev[s] = {pairs[s].x, pairs[s].y};
+    st = upload_erasures(pl, ev.data(), num_stripes, s_k);
+    if (st != RAID6C_OK) return st;
+  }
+  // order after anything already queued on the plan stream
+  ZP_CUDA(cudaEventRecord(pl->ev_out[0], pl->stream));
+  ZP_CUDA(cudaStreamWaitEvent(s_in, pl->ev_out[0], 0));
+  ZP_CUDA(cudaEventRecord(pl->ev_out[1], pl->stream));
+  uint64_t h2d = 0, d2h = 0;
+  int c = 0;
+  for (int s0 = 0; s0 < num_stripes; s0 += cs, c++) {
+    const int slot = c & 1;
+    const int ns = std::min(cs, num_stripes - s0);
+    uint8_t* base = pl->d_stage + static_cast<size_t>(slot) * pl->slot_bytes;
+    uint8_t* dP = base + static_cast<size_t>(cs) * N * sd;
+    uint8_t* dQ = dP + static_cast<size_t>(cs) * sp;
+    const size_t dstripe = static_cast<size_t>(N) * sd;
+    if (c >= 2) ZP_CUDA(cudaStreamWaitEvent(s_in, pl->ev_out[slot], 0));
+    // ---- H2D of the inputs
+    for (int i = 0; i < ns; i++) {
+      const int s = s0 + i;
+      const uint8_t* hd = data + static_cast<size_t>(s) * stripe_stride;
+      uint8_t* dd = base + static_cast<size_t>(i) * dstripe;
+      int x = N, y = N + 1;
+      if (recover) { x = pairs[s].x; y = pairs[s].y; }
+      // contiguous runs of surviving data strips
+      int k = 0;
+      while (k < N) {
+        if (k == x || k == y) { k++; continue; }
+        int e = k;
+        while (e < N && e != x && e != y) e++;
+        st = copy_rows(dd + static_cast<size_t>(k) * sd, sd, hd + static_cast<size_t>(k) * strip_stride, strip_stride,
+                       pl->bytes, e - k, cudaMemcpyHostToDevice, s_in);
+        if (st != RAID6C_OK) return st;
+        h2d += static_cast<uint64_t>(e - k) * pl->bytes;
+        k = e;
+      }
+      if (recover && x != N && y != N) {
+        ZP_CUDA(cudaMemcpyAsync(dP + static_cast<size_t>(i) * sp, P + static_cast<size_t>(s) * parity_stride, pl->pbytes,
+                                cudaMemcpyHostToDevice, s_in));
+        h2d += pl->pbytes;
+      }
+      if (recover && y != N + 1) {
+        ZP_CUDA(cudaMemcpyAsync(dQ + static_cast<size_t>(i) * sp, Q + static_cast<size_t>(s) * parity_stride, pl->pbytes,
+                                cudaMemcpyHostToDevice, s_in));
+        h2d += pl->pbytes;
+      }
+    }
+    ZP_CUDA(cudaEventRecord(pl->ev_in[slot], s_in));
+    // ---- kernel
+    ZP_CUDA(cudaStreamWaitEvent(s_k, pl->ev_in[slot], 0));
+    zp::ZpArgs a;
+    std::memset(&a, 0, sizeof(a));
+    for (int k = 0; k < N; k++) a.base[k] = base + static_cast<size_t>(k) * sd;
+    a.base[N] = dP;
+    a.base[N + 1] = dQ;
+    a.data_stride = dstripe;
+    a.parity_stride = sp;
+    a.num_stripes = ns;
+    a.ei = N;
+    a.ej = N + 1;
+    if (recover) {
+      a.er = pl->d_er + s0;
+      a.er_stride = 1;
+    }
+    st = launch(pl, a, recover, s_k);
+    if (st != RAID6C_OK) return st;
+    ZP_CUDA(cudaEventRecord(pl->ev_k[slot], s_k));
+    // ---- D2H of the outputs
+    ZP_CUDA(cudaStreamWaitEvent(s_out, pl->ev_k[slot], 0));
+    if (!recover) {
+      st = copy_rows(P + static_cast<size_t>(s0) * parity_stride, parity_stride, dP, sp, pl->pbytes, ns,
+                     cudaMemcpyDeviceToHost, s_out);
+      if (st != RAID6C_OK) return st;
+      st = copy_rows(Q + static_cast<size_t>(s0) * parity_stride, parity_stride, dQ, sp, pl->pbytes, ns,
+                     cudaMemcpyDeviceToHost, s_out);
+      if (st != RAID6C_OK) return st;
+      d2h += 2ull * ns * pl->pbytes;
+    } else {
+      for (int i = 0; i < ns; i++) {
+        const int s = s0 + i;
+        const int lost[2] = {pairs[s].x, pairs[s].y};
+        for (int q = 0; q < 2; q++) {
+          const int k = lost[q];
+          if (k < N) {
+            ZP_CUDA(cudaMemcpyAsync(data + static_cast<size_t>(s) * stripe_stride + static_cast<size_t>(k) * strip_stride,
+                                    base + static_cast<size_t>(i) * dstripe + static_cast<size_t>(k) * sd, pl->bytes,
+                                    cudaMemcpyDeviceToHost, s_out));
+            d2h += pl->bytes;
+          } else {
+            uint8_t* hdst = (k == N ? P : Q) + static_cast<size_t>(s) * parity_stride;
+            const uint8_t* dsrc = (k == N ? dP : dQ) + static_cast<size_t>(i) * sp;
+            ZP_CUDA(cudaMemcpyAsync(hdst, dsrc, pl->pbytes, cudaMemcpyDeviceToHost, s_out));
+            d2h += pl->pbytes;
+          }
+        }
+      }
+    }
+    ZP_CUDA(cudaEventRecord(pl->ev_out[slot], s_out));
+  }
+  ZP_CUDA(cudaStreamSynchronize(s_out));
+  ZP_CUDA(cudaStreamSynchronize(s_k));
+  ZP_CUDA(cudaGetLastError());
+  pl->h2d = h2d;
+  pl->d2h = d2h;
+  return RAID6C_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+size_t raid6c_word_count(int p, size_t bytes) { return is_valid_p(p) ? word_count(p, bytes) : 0; }
+size_t raid6c_parity_bytes(int p, size_t bytes) { return is_valid_p(p) ? parity_bytes(p, bytes) : 0; }
+int raid6c_valid_p(int p) { return is_valid_p(p) ? 1 : 0; }
+int raid6c_has_fast_path(int p) { return zp::fast_entry(p) != nullptr ? 1 : 0; }
+uint64_t raid6c_launch_count(void) { return g_launches.load(); }
+const char* raid6c_last_cuda_error(void) { return g_last_err.c_str(); }
+
+const char* raid6c_status_string(raid6c_status s) {
+  switch (s) {
+    case RAID6C_OK: return "ok";
+    case RAID6C_E_INVALID_P: return "p is not an odd prime in [3, 257]";
+    case RAID6C_E_INVALID_N: return "N must satisfy 1 <= N <= p";
+    case RAID6C_E_INVALID_INDEX: return "lost strip index out of range or repeated";
+    case RAID6C_E_NULL: return "null pointer argument";
+    case RAID6C_E_SIZE: return "invalid size or stride";
+    case RAID6C_E_CUDA: return "CUDA error";
+    case RAID6C_E_NO_DEVICE: return "no usable sm_100 CUDA device";
+    case RAID6C_E_PLAN: return "call does not match the plan";
+  }
+  return "unknown status";
+}
+
+raid6c_status raid6c_plan_create(raid6c_plan* out, int p, int N, size_t bytes, int device, void* stream) {
+  if (!out) return RAID6C_E_NULL;
+  *out = nullptr;
+  raid6c_plan pl = new raid6c_plan_s();
+  raid6c_status st = plan_init(pl, p, N, bytes, device, static_cast<cudaStream_t>(stream));
+  if (st != RAID6C_OK) {
+    delete pl;
+    return st;
+  }
+  *out = pl;
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_plan_destroy(raid6c_plan plan) {
+  if (!plan) return RAID6C_E_NULL;
+  {
+    DeviceGuard g(plan->device);
+    cudaStreamSynchronize(plan->stream);
+    for (int i = 0; i < 3; i++)
+      if (plan->hs[i]) cudaStreamSynchronize(plan->hs[i]);
+  }
+  plan_release(plan);
+  delete plan;
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_plan_set_stream(raid6c_plan plan, void* stream) {
+  if (!plan) return RAID6C_E_NULL;
+  plan->stream = static_cast<cudaStream_t>(stream);
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_sync(raid6c_plan plan) {
+  if (!plan) return RAID6C_E_NULL;
+  DeviceGuard g(plan->device);
+  cudaError_t e = cudaStreamSynchronize(plan->stream);
+  raid6c_status st = plan->sticky;
+  plan->sticky = RAID6C_OK;
+  if (e != cudaSuccess) return cuda_fail(e);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  return st;
+}
+
+raid6c_status raid6c_encode(int p, int N, const uint8_t* const* strips, uint8_t* P, uint8_t* Q, size_t bytes) {
+  if (!is_valid_p(p)) return RAID6C_E_INVALID_P;
+  if (N < 1 || N > p) return RAID6C_E_INVALID_N;
+  if (bytes == 0) return RAID6C_E_SIZE;
+  if (!strips || !P || !Q) return RAID6C_E_NULL;
+  for (int k = 0; k < N; k++)
+    if (!strips[k]) return RAID6C_E_NULL;
+  raid6c_plan pl;
+  raid6c_status st = cached_plan(p, N, bytes, &pl);
+  if (st != RAID6C_OK) return st;
+  zp::ZpArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int k = 0; k < N; k++) a.base[k] = strips[k];
+  a.base[N] = P;
+  a.base[N + 1] = Q;
+  a.num_stripes = 1;
+  a.ei = N;
+  a.ej = N + 1;
+  st = launch(pl, a, false, nullptr);
+  if (st != RAID6C_OK) return st;
+  ZP_CUDA(cudaStreamSynchronize(nullptr));
+  ZP_CUDA(cudaGetLastError());
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* const* strips, size_t bytes) {
+  if (!is_valid_p(p)) return RAID6C_E_INVALID_P;
+  if (N < 1 || N > p) return RAID6C_E_INVALID_N;
+  if (bytes == 0) return RAID6C_E_SIZE;
+  raid6c_status st = check_erasure(N, lost_i, lost_j);
+  if (st != RAID6C_OK) return st;
+  if (!strips) return RAID6C_E_NULL;
+  for (int k = 0; k < N + 2; k++)
+    if (!strips[k]) return RAID6C_E_NULL;
+  raid6c_plan pl;
+  st = cached_plan(p, N, bytes, &pl);
+  if (st != RAID6C_OK) return st;
+  zp::ZpArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int k = 0; k < N + 2; k++) a.base[k] = strips[k];
+  a.num_stripes = 1;
+  a.ei = std::min(lost_i, lost_j);
+  a.ej = std::max(lost_i, lost_j);
+  st = launch(pl, a, true, nullptr);
+  if (st != RAID6C_OK) return st;
+  ZP_CUDA(cudaStreamSynchronize(nullptr));
+  ZP_CUDA(cudaGetLastError());
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_encode_strided(raid6c_plan plan, const uint8_t* data, size_t strip_stride, size_t stripe_stride,
+                                    uint8_t* P, uint8_t* Q, size_t parity_stride, int num_stripes) {
+  zp::ZpArgs a;
+  raid6c_status st = strided_args(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, a);
+  if (st != RAID6C_OK) return st;
+  DeviceGuard g(plan->device);
+  return launch(plan, a, false, plan->stream);
+}
+
+raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t* data, size_t strip_stride, size_t stripe_stride,
+                                     uint8_t* P, uint8_t* Q, size_t parity_stride, int num_stripes,
+                                     const raid6c_erasure* erasures, int num_erasures, int erasures_on_device) {
+  zp::ZpArgs a;
+  raid6c_status st = strided_args(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, a);
+  if (st != RAID6C_OK) return st;
+  if (!erasures) return RAID6C_E_NULL;
+  if (num_erasures != 1 && num_erasures != num_stripes) return RAID6C_E_SIZE;
+  DeviceGuard g(plan->device);
+  if (erasures_on_device) {
+    a.er = reinterpret_cast<const int2*>(erasures);
+    a.er_stride = num_erasures == 1 ? 0 : 1;
+  } else if (num_erasures == 1) {
+    st = check_erasure(plan->N, erasures[0].lost_i, erasures[0].lost_j);
+    if (st != RAID6C_OK) return st;
+    a.ei = std::min(erasures[0].lost_i, erasures[0].lost_j);
+    a.ej = std::max(erasures[0].lost_i, erasures[0].lost_j);
+  } else {
+    for (int s = 0; s < num_erasures; s++) {
+      st = check_erasure(plan->N, erasures[s].lost_i, erasures[s].lost_j);
+      if (st != RAID6C_OK) return st;
+    }
+    st = upload_erasures(plan, erasures, num_erasures, plan->stream);
+    if (st != RAID6C_OK) return st;
+    a.er = plan->d_er;
+    a.er_stride = 1;
+  }
+  return launch(plan, a, true, plan->stream);
+}
+
+raid6c_status raid6c_encode_host(raid6c_plan plan, const uint8_t* data, size_t strip_stride, size_t stripe_stride,
+                                 uint8_t* P, uint8_t* Q, size_t parity_stride, int num_stripes) {
+  return host_run(plan, const_cast<uint8_t*>(data), strip_stride, stripe_stride, P, Q, parity_stride, num_stripes,
+                  nullptr, 0, false);
+}
+
+raid6c_status raid6c_recover_host(raid6c_plan plan, uint8_t* data, size_t strip_stride, size_t stripe_stride,
+                                  uint8_t* P, uint8_t* Q, size_t parity_stride, int num_stripes,
+                                  const raid6c_erasure* erasures, int num_erasures) {
+  return host_run(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, erasures, num_erasures,
+                  true);
+}
+
+raid6c_status raid6c_host_traffic(raid6c_plan plan, uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
+  if (!plan || !h2d_bytes || !d2h_bytes) return RAID6C_E_NULL;
+  *h2d_bytes = plan->h2d;
+  *d2h_bytes = plan->d2h;
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_fill(uint8_t* dst, size_t strip_stride, size_t stripe_stride, size_t len, int nstrips,
+                          int nstripes, uint64_t seed, int cfg, int stripe0, int strip0, int sparse_mode,
+                          void* stream) {
+  if (!dst) return RAID6C_E_NULL;
+  if (nstrips < 0 || nstripes < 0) return RAID6C_E_SIZE;
+  if (len == 0 || nstrips == 0 || nstripes == 0) return RAID6C_OK;
+  cudaError_t e = zp::harness_fill(dst, strip_stride, stripe_stride, len, nstrips, nstripes, seed, cfg, stripe0, strip0,
+                                   sparse_mode, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_count_mismatch(const uint8_t* a, const uint8_t* b, size_t len, uint64_t* count_dev, void* stream) {
+  if (!a || !b || !count_dev) return RAID6C_E_NULL;
+  if (len == 0) return RAID6C_OK;
+  cudaError_t e = zp::harness_count_mismatch(a, b, len, count_dev, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return RAID6C_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// zp_args.h -- launch descriptor shared by the host side of libraid6c and its kernels.
+// (Product code only; nothing here is shared with oracle/.)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "raid6c.h"
+
+namespace zp {
+
+// One launch = a batch of stripes with a common (p, N, bytes).  Strip k of stripe s lives
+// at base[k] + s * (k < N ? data_stride : parity_stride).
+struct ZpArgs {
+  const uint8_t* base[RAID6C_MAX_STRIPS];
+  uint64_t data_stride;
+  uint64_t parity_stride;
+  uint64_t bytes;   // data strip length
+  uint64_t pbytes;  // parity strip length (W*n bits rounded up to bytes)
+  int N;
+  int num_stripes;
+  // Erasure pair per stripe: er[s] if er != nullptr, else (ei, ej).  Encode = (N, N+1).
+  const int2* er;
+  int er_stride;  // er[s * er_stride] (0 = one pair for every stripe)
+  int ei, ej;
+  // Work split (set by the host per kernel geometry):
+  //   body: tiles [0, body_tiles) of every strip, TB bytes each, all via TMA;
+  //   tail: bytes [body_tiles*TB, pbytes) via direct loads, chunk_bytes per unit.
+  uint64_t body_tiles;
+  uint64_t tail_units_per_stripe;
+};
+
+// Kernel-geometry record for one compiled prime (fast path) -- filled by each
+// instantiation translation unit and used by the host to split work and launch.
+struct FastEntry {
+  int p;
+  int chunk_bytes;  // bytes per thread-chunk (whole periods of lcm(n,32) bits)
+  int tile_bytes;   // TMA row bytes = consumer threads * chunk_bytes
+  int threads;      // consumer threads (+32 producer threads per CTA)
+  size_t smem_bytes;
+  const void* enc_kernel;  // __global__ void(ZpArgs)
+  const void* rec_kernel;
+};
+
+const FastEntry* fast_entry(int p);  // nullptr if p has no fast path
+
+// Generic (runtime-p) kernels, any odd prime <= 257.
+cudaError_t generic_launch(const ZpArgs& a, int p, bool recover, cudaStream_t st, int num_sms);
+
+}  // namespace zp

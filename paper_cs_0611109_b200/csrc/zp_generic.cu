@@ -1,0 +1,208 @@
+// zp_generic.cu -- runtime-p Z_p-RAID kernel (any odd prime p <= 257) for primes without a
+// compile-time specialisation (zp_fast.cuh).  Same mathematics, simplest mapping:
+//   * one thread per byte-aligned group of g = 8/gcd(n,8) words (so outputs are whole bytes
+//     and no two threads touch the same byte);
+//   * each word is held as a p-bit value in up to 9 32-bit limbs (slot bit p-1 = the R'
+//     overflow), multiplication by x^a is a rotation of the p-bit slot, reduction pi is
+//     deferred to the end of each sum;
+//   * the class epilogues are the same as the fast path (Lemma 23.2 proof PAPER.md:380-401,
+//     Sec. 4.6), the DD inverse by the same doubling chain.
+// Correctness path: no TMA, no shared memory; used for primes outside the fast set.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "zp_args.h"
+
+namespace zp {
+namespace {
+
+constexpr int NL = 9;  // limbs for p <= 257 bits (bit 256 = slot overflow of p = 257)
+
+struct Word {
+  uint32_t v[NL];
+};
+
+__device__ __forceinline__ void wzero(Word& w) {
+#pragma unroll
+  for (int i = 0; i < NL; i++) w.v[i] = 0;
+}
+__device__ __forceinline__ void wxor(Word& a, const Word& b) {
+#pragma unroll
+  for (int i = 0; i < NL; i++) a.v[i] ^= b.v[i];
+}
+__device__ __forceinline__ int wbit(const Word& w, int j) { return (w.v[j >> 5] >> (j & 31)) & 1; }
+__device__ __forceinline__ void wflip(Word& w, int j) { w.v[j >> 5] ^= 1u << (j & 31); }
+
+// Bit `pos` of a strip of `len` bytes (zero past the end).
+__device__ __forceinline__ uint32_t sbit(const uint8_t* g, uint64_t len, uint64_t pos) {
+  const uint64_t byte = pos >> 3;
+  return byte < len ? (g[byte] >> (pos & 7)) & 1u : 0u;
+}
+
+__device__ void load_word(const uint8_t* g, uint64_t len, uint64_t w, int n, Word& out) {
+  wzero(out);
+  const uint64_t b0 = w * static_cast<uint64_t>(n);
+  if ((b0 >> 3) >= len) return;
+  for (int j = 0; j < n; j++)
+    if (sbit(g, len, b0 + j)) wflip(out, j);
+}
+
+// acc ^= rot_a(src) inside the p-bit slot (src has slot bit p-1 clear).
+__device__ void rot_acc(Word& acc, const Word& src, int a, int p) {
+  const int n = p - 1;
+  for (int j = 0; j < n; j++) {
+    if (!wbit(src, j)) continue;
+    int t = j + a;
+    if (t >= p) t -= p;
+    wflip(acc, t);
+  }
+}
+
+// pi: if slot bit p-1 is set flip bits 0..n-1; clear bit p-1.
+__device__ void reduce(Word& w, int p) {
+  const int n = p - 1;
+  if (wbit(w, n)) {
+    wflip(w, n);
+    for (int j = 0; j < n; j++) wflip(w, j);
+  }
+}
+
+struct Desc {
+  int x, y, cls, base;
+};
+
+__device__ Desc desc_of(const ZpArgs& a, int s, bool recover) {
+  int i = a.N, j = a.N + 1;
+  if (recover) {
+    if (a.er) {
+      const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
+      i = e.x; j = e.y;
+    } else {
+      i = a.ei; j = a.ej;
+    }
+  }
+  Desc d;
+  d.x = i < j ? i : j;
+  d.y = i < j ? j : i;
+  if (d.y == a.N + 1) d.cls = (d.x == a.N) ? 0 : 1;  // PQ : DQ
+  else d.cls = (d.y == a.N) ? 2 : 3;                  // DP : DD
+  d.base = (d.cls >= 2) ? d.x : 0;
+  return d;
+}
+
+__device__ __forceinline__ uint64_t sstride(const ZpArgs& a, int k) { return k < a.N ? a.data_stride : a.parity_stride; }
+
+constexpr int GROUP_MAX_BYTES = 128;  // g*n/8 <= n/2 <= 128
+
+__global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int recover) {
+  const int n = p - 1;
+  const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);  // 8 / gcd(n, 8)
+  const int gbytes = g * n / 8;
+  const uint64_t W = (8 * a.bytes + n - 1) / n;
+  const uint64_t groups = (W + g - 1) / g;
+  const uint64_t total = groups * static_cast<uint64_t>(a.num_stripes);
+  for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
+       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(u / groups);
+    const uint64_t grp = u - static_cast<uint64_t>(s) * groups;
+    const Desc d = desc_of(a, s, recover != 0);
+    int k0, k1;
+    if (d.cls == 0) { k0 = a.N; k1 = a.N + 1; }
+    else if (d.cls == 1) { k0 = d.x; k1 = a.N + 1; }
+    else if (d.cls == 2) { k0 = d.x; k1 = a.N; }
+    else { k0 = d.x; k1 = d.y; }
+    uint8_t ob0[GROUP_MAX_BYTES], ob1[GROUP_MAX_BYTES];
+    for (int i = 0; i < gbytes; i++) { ob0[i] = 0; ob1[i] = 0; }
+    for (int wi = 0; wi < g; wi++) {
+      const uint64_t w = grp * g + wi;
+      Word Pa, acc, L, o0, o1;
+      wzero(Pa);
+      wzero(acc);
+      for (int r = 0; r < a.N; r++) {
+        int k = r;
+        if (k >= d.x) k++;
+        if (k >= d.y) k++;
+        const uint64_t len = k < a.N ? a.bytes : a.pbytes;
+        load_word(a.base[k] + static_cast<uint64_t>(s) * sstride(a, k), len, w, n, L);
+        if (k <= a.N) wxor(Pa, L);
+        if (k != a.N) {
+          int amt = ((k < a.N ? k : p) - d.base) % p;
+          if (amt < 0) amt += p;
+          rot_acc(acc, L, amt, p);
+        }
+      }
+      if (d.cls == 0) {
+        o0 = Pa;
+        reduce(acc, p);
+        o1 = acc;
+      } else if (d.cls == 1) {
+        o0 = Pa;
+        rot_acc(acc, Pa, d.x, p);
+        reduce(acc, p);
+        o1 = acc;
+      } else if (d.cls == 2) {
+        reduce(acc, p);
+        o0 = acc;
+        o1 = Pa;
+        wxor(o1, o0);
+      } else {
+        wxor(acc, Pa);
+        reduce(acc, p);
+        const Word t = acc;
+        Word S = t;
+        const int M = (p + 1) / 2;
+        const int bz = (2 * (d.y - d.x)) % p;
+        int top = 31 - __clz(M);
+        int m = 1;
+        for (int bit = top - 1; bit >= 0; bit--) {
+          Word nx = S;
+          rot_acc(nx, S, (bz * m) % p, p);
+          reduce(nx, p);
+          S = nx;
+          m *= 2;
+          if ((M >> bit) & 1) {
+            nx = S;
+            rot_acc(nx, t, (bz * m) % p, p);
+            reduce(nx, p);
+            S = nx;
+            m += 1;
+          }
+        }
+        o1 = S;
+        o0 = S;
+        wxor(o0, Pa);
+      }
+      for (int j = 0; j < n; j++) {
+        const int bpos = wi * n + j;
+        ob0[bpos >> 3] |= static_cast<uint8_t>(wbit(o0, j) << (bpos & 7));
+        ob1[bpos >> 3] |= static_cast<uint8_t>(wbit(o1, j) << (bpos & 7));
+      }
+    }
+    const uint64_t byte0 = grp * static_cast<uint64_t>(gbytes);
+    uint8_t* g0 = const_cast<uint8_t*>(a.base[k0]) + static_cast<uint64_t>(s) * sstride(a, k0);
+    uint8_t* g1 = const_cast<uint8_t*>(a.base[k1]) + static_cast<uint64_t>(s) * sstride(a, k1);
+    const uint64_t len0 = k0 < a.N ? a.bytes : a.pbytes, len1 = k1 < a.N ? a.bytes : a.pbytes;
+    for (int i = 0; i < gbytes; i++) {
+      if (byte0 + i < len0) g0[byte0 + i] = ob0[i];
+      if (byte0 + i < len1) g1[byte0 + i] = ob1[i];
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t generic_launch(const ZpArgs& a, int p, bool recover, cudaStream_t st, int num_sms) {
+  const int n = p - 1;
+  const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);
+  const uint64_t W = (8 * a.bytes + n - 1) / n;
+  const uint64_t total = ((W + g - 1) / g) * static_cast<uint64_t>(a.num_stripes);
+  const int threads = 128;
+  uint64_t blocks = (total + threads - 1) / threads;
+  const uint64_t cap = static_cast<uint64_t>(num_sms) * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  zp_generic_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(a, p, recover ? 1 : 0);
+  return cudaGetLastError();
+}
+
+}  // namespace zp

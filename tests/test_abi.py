@@ -1,0 +1,60 @@
+"""CPU-side checks of the C-ABI library: it loads without a GPU, exports every symbol that
+include/raid6c.h declares, and its host-only helpers agree with the oracle's size rules.
+(No compute call is made here; parity tests are in test_gpu_parity.py.)"""
+import os
+import re
+import subprocess
+
+import pytest
+
+import oracle
+from paper_cs_0611109_b200 import raid6c as R
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "raid6c.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(raid6c_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    names = _declared()
+    assert len(names) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", R.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\b(raid6c_[a-z0-9_]+)\b", out))
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    assert set(R.EXPORTED) == set(names)
+
+
+def test_sizes_agree_with_oracle():
+    for p in [3, 5, 7, 13, 17, 59, 61, 97, 257]:
+        for nb in [1, 2, 3, 7, 100, 4097, 65536, 4 << 20]:
+            assert R.word_count(p, nb) == oracle.word_count(p, nb)
+            assert R.parity_bytes(p, nb) == oracle.parity_bytes(p, nb)
+    assert R.parity_bytes(9, 100) == 0 and R.word_count(4, 10) == 0
+
+
+def test_valid_p_and_fast_set():
+    primes = [q for q in range(3, 258) if all(q % d for d in range(2, int(q ** 0.5) + 1))]
+    for q in range(0, 300):
+        assert R.valid_p(q) == (q in primes and q >= 3 and q <= 257)
+    for q in [5, 13, 59, 61, 257]:
+        assert R.has_fast_path(q)
+
+
+def test_status_strings():
+    for st in range(9):
+        assert R._lib.raid6c_status_string(st)
+
+
+def test_no_device_is_reported_not_faked():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(R.Raid6Error, match="NO_DEVICE"):
+        R.Plan(13, 12, 4096)
+    with pytest.raises(R.Raid6Error):
+        R.encode(13, 1, [0], 0, 0, 16)  # NULL pointers are rejected before any device call

@@ -1,0 +1,324 @@
+"""GPU parity tests: libraid6c (through its C ABI) vs the CPU oracle, bit-exact.
+
+Sizes the oracle finishes in seconds (spanning several TMA tiles plus a ragged tail),
+every erasure pair for small N, unaligned pointers, the generic (runtime-p) kernel, and at
+BASELINE.json's full sizes -- in bench.py's launch configuration -- sampled word-aligned
+segments checked against the oracle plus whole-strip round-trip equality with the
+generator's bytes.  All inputs are seeded (synthetic/)."""
+import itertools
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes but never run there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import synthetic  # noqa: E402
+from paper_cs_0611109_b200 import raid6c as R  # noqa: E402
+from tests.gpu_util import Batch, segment_bounds  # noqa: E402
+
+FAST = [3, 5, 7, 13, 17, 59, 61, 257]
+GENERIC = [11, 19, 23, 29, 31, 37, 97]
+
+
+def _poison(b, s, ks):
+    for k in ks:
+        b.strip(s, k).fill_(0xA5)
+
+
+def _np(t):
+    return t.cpu().numpy()
+
+
+# ------------------------------------------------------------------ generator
+def test_fill_matches_numpy_generator():
+    for mode, nbytes, S in [(0, 1000, 3), (1, 4099, 2), (2, 777, 4)]:
+        b = Batch(13, 5, nbytes, S)
+        b.fill_synthetic(seed=7, cfg=3, stripe0=11, sparse_mode=mode)
+        torch.cuda.synchronize()
+        for s in range(S):
+            sparse = mode == 1 or (mode == 2 and (11 + s) % 2 == 1)
+            for k in range(5):
+                ref = synthetic.strip_bytes(7, 3, 11 + s, k, nbytes, sparse)
+                assert np.array_equal(_np(b.strip(s, k)), ref), (mode, s, k)
+
+
+# ------------------------------------------------------------------ north-star single-stripe API
+@pytest.mark.parametrize("p", FAST + GENERIC)
+def test_encode_single_matches_oracle(p):
+    rng = np.random.default_rng(p)
+    for N, nbytes in [(1, 1), (min(p, 3), 37), (p - 1, 5000), (p, 1024 + 7)]:
+        if p == 257 and N > 70:
+            N = 64
+        data = [rng.integers(0, 256, nbytes, dtype=np.uint8) for _ in range(N)]
+        P, Q = oracle.encode(p, data, nbytes)
+        pb = R.parity_bytes(p, nbytes)
+        dd = [torch.from_numpy(d).cuda() for d in data]
+        gP = torch.full((pb,), 0x5A, dtype=torch.uint8, device="cuda")
+        gQ = torch.full((pb,), 0x5A, dtype=torch.uint8, device="cuda")
+        R.encode(p, N, dd, gP, gQ, nbytes)
+        assert np.array_equal(_np(gP), P), (p, N, nbytes)
+        assert np.array_equal(_np(gQ), Q), (p, N, nbytes)
+
+
+@pytest.mark.parametrize("p,N,nbytes", [(3, 3, 100), (5, 4, 65536), (7, 7, 999), (13, 12, 3 * 12288 + 4097),
+                                        (17, 17, 2000), (59, 9, 30000), (61, 11, 16000), (257, 6, 20000),
+                                        (11, 10, 1500), (29, 5, 777)])
+def test_recover_single_all_pairs(p, N, nbytes):
+    rng = np.random.default_rng(p * 7 + N)
+    data = [rng.integers(0, 256, nbytes, dtype=np.uint8) for _ in range(N)]
+    P, Q = oracle.encode(p, data, nbytes)
+    orig = data + [P, Q]
+    pairs = list(itertools.combinations(range(N + 2), 2))
+    if len(pairs) > 40:
+        pairs = pairs[:10] + [pairs[i] for i in rng.choice(len(pairs), 30, replace=False)]
+    for i, j in pairs:
+        strips = [torch.from_numpy(a.copy()).cuda() for a in orig]
+        strips[i].fill_(0xA5)
+        strips[j].fill_(0x5A)
+        R.recover(p, N, j, i, strips, nbytes)
+        for k in (i, j):
+            assert np.array_equal(_np(strips[k]), orig[k]), (p, N, i, j, k)
+
+
+# ------------------------------------------------------------------ batched / strided API (TMA path)
+@pytest.mark.parametrize("p,N,nbytes,S", [(13, 12, 5 * 12288 + 1234, 3), (5, 4, 4 * 12288 + 4096, 2),
+                                          (59, 58, 3 * 14848 + 99, 2), (61, 60, 2 * 15360 + 7, 2),
+                                          (257, 64, 3 * 8192 + 5000, 2), (3, 3, 12288 * 3 + 1, 2),
+                                          (17, 16, 12288 * 2 + 30, 2), (7, 6, 12288 * 2 + 13, 2),
+                                          (19, 18, 9000, 2)])
+def test_batch_encode_and_mixed_recover(p, N, nbytes, S):
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=1, cfg=9, stripe0=0)
+    b.par.fill_(0x77)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    refs = []
+    for s in range(S):
+        data = synthetic.stripe_strips(1, 9, s, N, nbytes)
+        P, Q = oracle.encode(p, data, nbytes)
+        assert np.array_equal(_np(b.strip(s, N)), P), (p, s)
+        assert np.array_equal(_np(b.strip(s, N + 1)), Q), (p, s)
+        refs.append(data + [P, Q])
+    # mixed classes across stripes, host pairs then device pairs
+    allp = synthetic.all_pairs(N)
+    rng = np.random.default_rng(p)
+    for trial in range(3):
+        pairs = [allp[int(rng.integers(len(allp)))] for _ in range(S)]
+        if trial == 0:
+            pairs[0] = (0, 1) if N >= 2 else (0, N)
+        for s, (i, j) in enumerate(pairs):
+            _poison(b, s, (i, j))
+        if trial == 2:
+            dev = torch.tensor(pairs, dtype=torch.int32, device="cuda")
+            plan.recover_strided(*b.args(), dev)
+        else:
+            plan.recover_strided(*b.args(), pairs)
+        plan.sync()
+        for s, (i, j) in enumerate(pairs):
+            for k in (i, j):
+                assert np.array_equal(_np(b.strip(s, k)), refs[s][k]), (p, trial, s, i, j, k)
+    plan.close()
+
+
+@pytest.mark.parametrize("offset", [1, 3, 8, 15])
+def test_unaligned_pointers(offset):
+    p, N, nbytes, S = 13, 12, 3 * 12288 + 5, 2
+    b = Batch(p, N, nbytes, S, offset=offset, align=0)
+    b.fill_synthetic(seed=2, cfg=1)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    for s in range(S):
+        data = synthetic.stripe_strips(2, 1, s, N, nbytes)
+        P, Q = oracle.encode(p, data, nbytes)
+        assert np.array_equal(_np(b.strip(s, N)), P)
+        assert np.array_equal(_np(b.strip(s, N + 1)), Q)
+        orig = data + [P, Q]
+        for (i, j) in [(0, 5), (3, N), (7, N + 1), (N, N + 1)]:
+            _poison(b, s, (i, j))
+            plan.recover_strided(*b.args(), [(i, j)] * 1)
+            plan.sync()
+            assert np.array_equal(_np(b.strip(s, i)), orig[i])
+            assert np.array_equal(_np(b.strip(s, j)), orig[j])
+
+
+def test_lost_strips_never_read_and_neighbours_untouched():
+    """Poisoned lost strips do not change the result; bytes outside the strips are untouched."""
+    p, N, nbytes, S = 13, 12, 2 * 12288 + 77, 2
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=3, cfg=2)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    # guard bytes between strips (stride padding) must stay as they are
+    b.data[:, :, nbytes:].fill_(0xEE)
+    b.par[:, :, b.pb:].fill_(0xEE)
+    snap = b.data.clone(), b.par.clone()
+    for fillv in (0x00, 0xFF, 0xA5):
+        for s in range(S):
+            b.strip(s, 2).fill_(fillv)
+            b.strip(s, 9).fill_(fillv)
+        plan.recover_strided(*b.args(), [(2, 9)])
+        plan.sync()
+        assert torch.equal(b.data, snap[0]) and torch.equal(b.par, snap[1])
+
+
+# ------------------------------------------------------------------ host-buffer API (e2e path)
+def test_host_buffer_api_matches_device_path():
+    p, N, nbytes, S = 13, 12, 2 * 12288 + 901, 5
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=4, cfg=2)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    hd = b.data.cpu().pin_memory()
+    hp = torch.zeros_like(b.par, device="cpu").pin_memory()
+    plan.encode_batch(hd, hp)
+    assert torch.equal(hp[:, :, :b.pb], b.par[:, :, :b.pb].cpu())
+    h2d, d2h = plan.host_traffic()
+    assert h2d == S * N * nbytes and d2h == S * 2 * b.pb
+    pairs = [(0, 1), (4, N), (5, N + 1), (N, N + 1), (10, 11)]
+    ref_d, ref_p = hd.clone(), hp.clone()
+    for s, (i, j) in enumerate(pairs):
+        for k in (i, j):
+            if k < N:
+                hd[s, k, :nbytes] = 0xA5
+            else:
+                hp[s, k - N, :b.pb] = 0xA5
+    plan.recover_batch(hd, hp, pairs)
+    assert torch.equal(hd, ref_d) and torch.equal(hp[:, :, :b.pb], ref_p[:, :, :b.pb])
+
+
+# ------------------------------------------------------------------ argument errors (T1)
+def test_argument_errors_are_synchronous():
+    t = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(R.Raid6Error, match="INVALID_P"):
+        R.Plan(9, 3, 100)
+    with pytest.raises(R.Raid6Error, match="INVALID_N"):
+        R.Plan(5, 6, 100)
+    with pytest.raises(R.Raid6Error, match="SIZE"):
+        R.Plan(5, 2, 0)
+    plan = R.Plan(5, 2, 16)
+    with pytest.raises(R.Raid6Error, match="INVALID_INDEX"):
+        plan.recover_strided(t, 16, 32, t, int(t.data_ptr()) + 16, 32, 1, [(1, 1)])
+    with pytest.raises(R.Raid6Error, match="INVALID_INDEX"):
+        plan.recover_strided(t, 16, 32, t, int(t.data_ptr()) + 16, 32, 1, [(0, 4)])
+    with pytest.raises(R.Raid6Error, match="NULL"):
+        plan.encode_strided(0, 16, 32, t, t, 32, 1)
+    with pytest.raises(R.Raid6Error, match="INVALID_INDEX"):
+        R.recover(5, 2, 0, 0, [t, t, t, t], 16)
+    plan.sync()
+
+
+# ------------------------------------------------------------------ full BASELINE sizes (sampled)
+def _check_segments(b, p, N, nbytes, seed, cfg, stripes, sparse_of=lambda s: False):
+    for s in stripes:
+        for which in ("head", "mid", "tail"):
+            b0, b1 = segment_bounds(p, nbytes, which)
+            segs = [synthetic.strip_bytes(seed, cfg, s, k, nbytes, sparse_of(s), lo=b0, hi=b1) for k in range(N)]
+            P, Q = oracle.encode(p, segs, b1 - b0)
+            e = b0 + P.size
+            assert np.array_equal(_np(b.par[s, 0, b0:e]), P), (s, which)
+            assert np.array_equal(_np(b.par[s, 1, b0:e]), Q), (s, which)
+
+
+def _roundtrip_full(b, plan, pairs):
+    S = b.S
+    ref_d, ref_p = b.data.clone(), b.par.clone()
+    for s, (i, j) in enumerate(pairs):
+        _poison(b, s, (i, j))
+    plan.recover_strided(*b.args(), torch.tensor(pairs, dtype=torch.int32, device="cuda"))
+    plan.sync()
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    R.count_mismatch(b.data, ref_d, b.data.numel(), cnt)
+    R.count_mismatch(b.par, ref_p, b.par.numel(), cnt)
+    torch.cuda.synchronize()
+    assert int(cnt.item()) == 0
+
+
+def test_config1_full():
+    """c1: p=5, N=4, 64 KiB, seed 0: full oracle encode + all 15 pairs."""
+    p, N, nbytes = 5, 4, 65536
+    b = Batch(p, N, nbytes, 1)
+    b.fill_synthetic(seed=0, cfg=1)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    data = synthetic.stripe_strips(0, 1, 0, N, nbytes)
+    P, Q = oracle.encode(p, data, nbytes)
+    assert np.array_equal(_np(b.strip(0, N)), P) and np.array_equal(_np(b.strip(0, N + 1)), Q)
+    orig = data + [P, Q]
+    for i, j in synthetic.all_pairs(N):
+        _poison(b, 0, (i, j))
+        plan.recover_strided(*b.args(), [(i, j)])
+        plan.sync()
+        for k in range(N + 2):
+            assert np.array_equal(_np(b.strip(0, k)), orig[k]), (i, j, k)
+
+
+def test_config2_full_size_all_91_pairs():
+    """c2: p=13, N=12, 4 MiB strips; 8 stripes in bench.py's launch configuration; all 91 pairs
+    (stripe s takes pair (s + 8r) mod 91 in round r) round-trip exactly; sampled oracle segments."""
+    p, N, nbytes, S = 13, 12, 4 << 20, 8
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=0, cfg=2)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    _check_segments(b, p, N, nbytes, 0, 2, [0, 5])
+    allp = synthetic.all_pairs(N)
+    for r in range(12):
+        _roundtrip_full(b, plan, [allp[(s + 8 * r) % 91] for s in range(S)])
+
+
+def test_config3_p257_sweep_points():
+    """c3: p=257, N=64, encode at 64 KiB (full oracle) and 16 MiB (sampled)."""
+    p, N = 257, 64
+    for nbytes, S, full in [(64 << 10, 2, True), (16 << 20, 1, False)]:
+        b = Batch(p, N, nbytes, S)
+        b.fill_synthetic(seed=0, cfg=3)
+        plan = R.Plan(p, N, nbytes)
+        plan.encode_strided(*b.args())
+        plan.sync()
+        if full:
+            for s in range(S):
+                data = synthetic.stripe_strips(0, 3, s, N, nbytes)
+                P, Q = oracle.encode(p, data, nbytes)
+                assert np.array_equal(_np(b.strip(s, N)), P) and np.array_equal(_np(b.strip(s, N + 1)), Q)
+        else:
+            _check_segments(b, p, N, nbytes, 0, 3, [0])
+        _roundtrip_full(b, plan, [(3, 60)] * S)
+
+
+def test_config4_full_size_dd():
+    """c4: p=59, N=58, 8 MiB; even stripes uniform, odd sparse; DD pairs (s mod 1653)."""
+    p, N, nbytes, S = 59, 58, 8 << 20, 4
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=0, cfg=4, sparse_mode=2)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    _check_segments(b, p, N, nbytes, 0, 4, [0, 1], sparse_of=lambda s: s % 2 == 1)
+    dd = [(i, j) for i in range(N) for j in range(i + 1, N)]
+    assert len(dd) == 1653
+    _roundtrip_full(b, plan, [dd[s * 411 % 1653] for s in range(S)])
+
+
+def test_config5_full_size_degraded_stream():
+    """c5: p=61, N=60, 32 MiB; per-stripe seeded erasure pairs over all classes."""
+    p, N, nbytes, S = 61, 60, 32 << 20, 4
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=0, cfg=5)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    _check_segments(b, p, N, nbytes, 0, 5, [1])
+    pairs = [(3, 40), (7, N), (11, N + 1), (N, N + 1)]
+    _roundtrip_full(b, plan, pairs)
+    _roundtrip_full(b, plan, [synthetic.erasure_pair(0, 5, s, N) for s in range(S)])
