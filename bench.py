@@ -149,7 +149,11 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     c = CONFIGS[args.config]
-    p, N, nbytes, S = c["p"], c["N"], c["nbytes"], args.stripes or c["stripes"]
+    p, N, S = c["p"], c["N"], args.stripes or c["stripes"]
+    nbytes = args.strip_bytes or c["nbytes"]
+    if args.strip_bytes and not args.stripes and args.config == 3:  # c3 sweep: >= 4 GiB per point
+        S = max(1, -(-(4 << 30) // (N * nbytes)))
+    c = dict(c, desc=c["desc"] if not args.strip_bytes else f"{c['desc']} [strip {nbytes} B, {S} stripes]")
     pb = R.parity_bytes(p, nbytes)
     ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
     stripe0 = rank * S  # weak scaling: each rank owns distinct global stripes
@@ -218,6 +222,7 @@ def run_ours(args):
     verified = None
     if args.verify:
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize(dev)  # cnt is zeroed on torch's stream; the compare runs on `stream`
         if do_rec:
             # ref snapshot was taken after warm-up steps; data/parity must be bit-identical
             R.count_mismatch(data, ref_data, data.numel(), cnt, stream)
@@ -443,6 +448,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--stripes", type=int, default=0, help="override stripes per GPU per step")
+    ap.add_argument("--strip-bytes", type=int, default=0, help="override strip length (c3 sweep)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-verify", dest="verify", action="store_false")
     ap.add_argument("--no-oracle-check", dest="oracle_check", action="store_false")

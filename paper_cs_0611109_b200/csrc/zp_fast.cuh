@@ -466,10 +466,13 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32) zp_kernel(const __grid_c
       uint32_t L[C];
       mbar_wait(&full[stage], ph);
       ld_chunk_smem<C>(stages + (size_t)stage * TB + tid * CB, L);
+      fold_row<G>(a, d, k, L, mtab, Pa, acc);
+      // Release the stage only after every loaded lane has been consumed: an mbarrier.arrive
+      // issued right after the LDS does not wait for the loads to complete, and the producer's
+      // next TMA write (async proxy) can then overwrite the row under a lagging warp's reads.
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       if (++stage == ST) { stage = 0; ph ^= 1u; }
-      fold_row<G>(a, d, k, L, mtab, Pa, acc);
     }
     uint32_t o0[C], o1[C];
     int k0, k1;
