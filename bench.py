@@ -142,6 +142,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_cs_0611109_b200 import raid6c as R
+    from paper_cs_0611109_b200 import shard
 
     rank, world, local = _env_rank()
     torch.cuda.set_device(local)
@@ -156,7 +157,7 @@ def run_ours(args):
     c = dict(c, desc=c["desc"] if not args.strip_bytes else f"{c['desc']} [strip {nbytes} B, {S} stripes]")
     pb = R.parity_bytes(p, nbytes)
     ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
-    stripe0 = rank * S  # weak scaling: each rank owns distinct global stripes
+    stripe0 = shard.weak_range(rank, S)[0]  # weak scaling: each rank owns distinct global stripes
     stream = torch.cuda.Stream(device=dev)
     data = torch.empty((S, N, ss), dtype=torch.uint8, device=dev)
     par = torch.zeros((S, 2, ps), dtype=torch.uint8, device=dev)
@@ -213,10 +214,7 @@ def run_ours(args):
     elapsed_ms = t_start.elapsed_time(t_end)
     enc_ms = [ev[t][0].elapsed_time(ev[t][1]) for t in range(args.warmup, total_steps)]
     rec_ms = [ev[t][1].elapsed_time(ev[t][2]) for t in range(args.warmup, total_steps)]
-    if world > 1:
-        tt = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(tt.item())
+    elapsed_ms = shard.max_over_ranks(elapsed_ms, dev)
 
     # ---------------------------------------------------------------- verification
     verified = None
@@ -233,11 +231,8 @@ def run_ours(args):
         oracle_ok = None
         if rank == 0 and args.oracle_check:
             oracle_ok = oracle_sample_check(p, N, nbytes, args.config, c["sparse"], stripe0, par)
-        tot = torch.tensor([mism, checked], dtype=torch.int64, device=dev)
-        if world > 1:
-            dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        verified = {"mismatched_bytes": int(tot[0].item()), "checked_bytes": int(tot[1].item()),
-                    "oracle_segments_match": oracle_ok}
+        tot = shard.sum_over_ranks([mism, checked], dev)
+        verified = {"mismatched_bytes": tot[0], "checked_bytes": tot[1], "oracle_segments_match": oracle_ok}
         del ref_data, ref_par
 
     # ---------------------------------------------------------------- e2e (host buffers, public API)
@@ -321,12 +316,8 @@ def run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_list
             h2d, d2h = b1[0] + b2[0], b1[1] + b2[1]
     # correctness of the host path vs the device path (parity of the same stripes)
     same = bool(torch.equal(hp[:, :, :pb], par[:, :, :pb].cpu()))
-    tm = statistics.mean(times)
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([tm], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        tm = float(tt.item())
+    from paper_cs_0611109_b200 import shard
+    tm = shard.max_over_ranks(statistics.mean(times), dev)
     user = (1 + int(do_rec)) * N * nbytes * S * world
     return {"value": round(user / tm / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "s_per_step": round(tm, 4),
