@@ -392,7 +392,7 @@ __device__ __forceinline__ void finish(const ZpArgs& a, const ItemDesc& d, uint3
 
 // ------------------------------------------------------------------ the kernel
 template <int P, bool RECOVER>
-__global__ void __launch_bounds__(Geo<P>::THREADS + 32) zp_kernel(const __grid_constant__ ZpArgs a) {
+__global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __grid_constant__ ZpArgs a) {
   using G = Geo<P>;
   constexpr int C = G::C, CB = G::CB, TB = G::TB, NT = G::THREADS, ST = G::STAGES;
   extern __shared__ __align__(128) uint8_t smem[];
