@@ -40,40 +40,46 @@ def _stale(target, sources):
     return any(os.path.getmtime(s) > t for s in sources)
 
 
-def _compile(src, force, verbose):
-    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+def _compile(src, force, verbose, objdir=OBJ, defines=()):
+    obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
     if not force and not _stale(obj, [src] + _deps()):
         return obj, None
-    cmd = [NVCC] + ARCH + FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+    cmd = [NVCC] + ARCH + FLAGS + [f"-D{d}" for d in defines] + (["-Xptxas", "-v"] if verbose else []) + \
+        ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj, (r.stderr if verbose else None)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Build the library (``out``); ``defines`` builds an experiment variant in its own object dir."""
+    objdir = OBJ if not defines else os.path.join(ROOT, "build", "obj_" + "_".join(defines))
+    os.makedirs(objdir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     with cf.ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
-        res = list(ex.map(lambda s: _compile(s, force, verbose), srcs))
+        res = list(ex.map(lambda s: _compile(s, force or bool(defines), verbose, objdir, defines), srcs))
     objs = [o for o, _ in res]
     if verbose:
         for o, log in res:
             if log:
                 print(f"== {os.path.basename(o)}\n{log}", file=sys.stderr)
-    if force or _stale(LIB, objs):
-        tmp = LIB + f".tmp{os.getpid()}"
+    LIBO = out
+    if force or defines or _stale(LIBO, objs):
+        tmp = LIBO + f".tmp{os.getpid()}"
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, LIBO)
+    return LIBO
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--out", default=LIB)
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args()
-    print(build(a.force, a.verbose))
+    print(build(a.force, a.verbose, a.out, tuple(a.defines)))

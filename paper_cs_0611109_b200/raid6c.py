@@ -13,7 +13,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libraid6c.so")
+LIB_PATH = os.environ.get("RAID6C_LIB") or os.path.join(_HERE, "libraid6c.so")  # override: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
