@@ -142,6 +142,30 @@ raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t *data, size_t str
                                      const raid6c_erasure *erasures, int num_erasures,
                                      int erasures_on_device);
 
+/* ------------------------------------------------ around the path */
+
+/* Scrub: check both parity equations of Eq. (znparity) on every word of
+ * num_stripes stripes (same layout as raid6c_encode_strided; all strips are read, none
+ * written).  bad_words: DEVICE array of num_stripes uint32; entry s is overwritten with the
+ * number of words w of stripe s for which P_w != sum_i d_{i,w} or Q_w != sum_i x^i d_{i,w}.
+ * Stream-ordered. */
+raid6c_status raid6c_scrub_strided(raid6c_plan plan, const uint8_t *data, size_t strip_stride,
+                                   size_t stripe_stride, const uint8_t *P, const uint8_t *Q,
+                                   size_t parity_stride, int num_stripes, uint32_t *bad_words);
+
+/* Small write: in stripe s, data strip k_s (disks[s], or disks[0] for every stripe when
+ * num_disks == 1; 0 <= k_s < N) is replaced by the `bytes` at new_data + s*new_stride
+ * (DEVICE), and P, Q are updated in the same pass by linearity of Eq. (znparity):
+ *   P' = P + (d_k + d_k'),   Q' = Q + x^k (d_k + d_k').
+ * Reads old d_k, new d_k, P, Q; writes d_k, P, Q.  `disks` is HOST memory unless
+ * disks_on_device != 0 (then a DEVICE int32 array, already validated).  Stream-ordered.
+ * new_data must not overlap the stripe. */
+raid6c_status raid6c_update_strided(raid6c_plan plan, uint8_t *data, size_t strip_stride,
+                                    size_t stripe_stride, uint8_t *P, uint8_t *Q,
+                                    size_t parity_stride, int num_stripes, const uint8_t *new_data,
+                                    size_t new_stride, const int32_t *disks, int num_disks,
+                                    int disks_on_device);
+
 /* ------------------------------------------------ host-buffer calls (end-to-end path) */
 
 /* Same as the strided calls, but every pointer is HOST memory (pinned memory gives

@@ -103,7 +103,7 @@ struct raid6c_plan_s {
   cudaStream_t stream = nullptr;
   const zp::FastEntry* fe = nullptr;
   int num_sms = 148;
-  int occ_enc = 1, occ_rec = 1;
+  int occ[4] = {1, 1, 1, 1};  // CTAs per SM per kernel mode
   int2* d_er = nullptr;
   size_t er_cap = 0;
   raid6c_status sticky = RAID6C_OK;
@@ -157,10 +157,11 @@ raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, 
   pl->fe = zp::fast_entry(p);
   if (pl->fe) {
     DeviceGuard g(device);
-    raid6c_status st = kernel_occupancy(device, pl->fe->enc_kernel, pl->fe->threads + 32, pl->fe->smem_bytes, &pl->occ_enc);
-    if (st != RAID6C_OK) return st;
-    st = kernel_occupancy(device, pl->fe->rec_kernel, pl->fe->threads + 32, pl->fe->smem_bytes, &pl->occ_rec);
-    if (st != RAID6C_OK) return st;
+    for (int m = 0; m < 4; m++) {
+      raid6c_status st = kernel_occupancy(device, pl->fe->kernel[m], pl->fe->threads + 32, pl->fe->smem_bytes[m],
+                                          &pl->occ[m]);
+      if (st != RAID6C_OK) return st;
+    }
   }
   return RAID6C_OK;
 }
@@ -179,7 +180,8 @@ void plan_release(raid6c_plan pl) {
 }
 
 // Launch one batch (all stripes share p, N, bytes).  a.base / strides / erasures are set.
-raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, bool recover, cudaStream_t st) {
+// mode: zp::KMODE_ENCODE / RECOVER / SCRUB / UPDATE.
+raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
   if (a.num_stripes == 0) return RAID6C_OK;
   a.N = pl->N;
   a.bytes = pl->bytes;
@@ -190,6 +192,10 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, bool recover, cudaStream_t s
     bool aligned = true;
     for (int k = 0; k < pl->N + 2; k++) aligned &= (reinterpret_cast<uintptr_t>(a.base[k]) & 15u) == 0;
     if (a.num_stripes > 1) aligned &= (a.data_stride % 16 == 0) && (a.parity_stride % 16 == 0);
+    if (mode == zp::KMODE_UPDATE) {
+      aligned &= (reinterpret_cast<uintptr_t>(a.nbase) & 15u) == 0;
+      if (a.num_stripes > 1) aligned &= a.new_stride % 16 == 0;
+    }
     const uint64_t TB = static_cast<uint64_t>(fe->tile_bytes), CB = static_cast<uint64_t>(fe->chunk_bytes);
     a.body_tiles = aligned ? pl->bytes / TB : 0;
     const uint64_t body_end = a.body_tiles * TB;
@@ -197,14 +203,14 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, bool recover, cudaStream_t s
     const uint64_t items = a.body_tiles * static_cast<uint64_t>(a.num_stripes);
     const uint64_t tail_ctas =
         (a.tail_units_per_stripe * static_cast<uint64_t>(a.num_stripes) + fe->threads - 1) / fe->threads;
-    const uint64_t cap = static_cast<uint64_t>(pl->num_sms) * (recover ? pl->occ_rec : pl->occ_enc);
+    const uint64_t cap = static_cast<uint64_t>(pl->num_sms) * pl->occ[mode];
     uint64_t grid = std::min<uint64_t>(cap, std::max<uint64_t>(items, tail_ctas));
     if (grid == 0) grid = 1;
     void* args[] = {&a};
-    err = cudaLaunchKernel(recover ? fe->rec_kernel : fe->enc_kernel, dim3(static_cast<unsigned>(grid)),
-                           dim3(fe->threads + 32), args, fe->smem_bytes, st);
+    err = cudaLaunchKernel(fe->kernel[mode], dim3(static_cast<unsigned>(grid)), dim3(fe->threads + 32), args,
+                           fe->smem_bytes[mode], st);
   } else {
-    err = zp::generic_launch(a, pl->p, recover, st, pl->num_sms);
+    err = zp::generic_launch(a, pl->p, mode, st, pl->num_sms);
   }
   if (err != cudaSuccess) {
     pl->sticky = RAID6C_E_CUDA;
@@ -439,7 +445,7 @@ raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_
       a.er = pl->d_er + s0;
       a.er_stride = 1;
     }
-    st = launch(pl, a, recover, s_k);
+    st = launch(pl, a, recover ? zp::KMODE_RECOVER : zp::KMODE_ENCODE, s_k);
     if (st != RAID6C_OK) return st;
     ZP_CUDA(cudaEventRecord(pl->ev_k[slot], s_k));
     // ---- D2H of the outputs
@@ -571,7 +577,7 @@ raid6c_status raid6c_encode(int p, int N, const uint8_t* const* strips, uint8_t*
   a.num_stripes = 1;
   a.ei = N;
   a.ej = N + 1;
-  st = launch(pl, a, false, nullptr);
+  st = launch(pl, a, zp::KMODE_ENCODE, nullptr);
   if (st != RAID6C_OK) return st;
   ZP_CUDA(cudaStreamSynchronize(nullptr));
   ZP_CUDA(cudaGetLastError());
@@ -596,7 +602,7 @@ raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* cons
   a.num_stripes = 1;
   a.ei = std::min(lost_i, lost_j);
   a.ej = std::max(lost_i, lost_j);
-  st = launch(pl, a, true, nullptr);
+  st = launch(pl, a, zp::KMODE_RECOVER, nullptr);
   if (st != RAID6C_OK) return st;
   ZP_CUDA(cudaStreamSynchronize(nullptr));
   ZP_CUDA(cudaGetLastError());
@@ -609,7 +615,7 @@ raid6c_status raid6c_encode_strided(raid6c_plan plan, const uint8_t* data, size_
   raid6c_status st = strided_args(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, a);
   if (st != RAID6C_OK) return st;
   DeviceGuard g(plan->device);
-  return launch(plan, a, false, plan->stream);
+  return launch(plan, a, zp::KMODE_ENCODE, plan->stream);
 }
 
 raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t* data, size_t strip_stride, size_t stripe_stride,
@@ -639,7 +645,55 @@ raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t* data, size_t str
     a.er = plan->d_er;
     a.er_stride = 1;
   }
-  return launch(plan, a, true, plan->stream);
+  return launch(plan, a, zp::KMODE_RECOVER, plan->stream);
+}
+
+raid6c_status raid6c_scrub_strided(raid6c_plan plan, const uint8_t* data, size_t strip_stride, size_t stripe_stride,
+                                   const uint8_t* P, const uint8_t* Q, size_t parity_stride, int num_stripes,
+                                   uint32_t* bad_words) {
+  zp::ZpArgs a;
+  raid6c_status st = strided_args(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, a);
+  if (st != RAID6C_OK) return st;
+  if (!bad_words) return RAID6C_E_NULL;
+  if (num_stripes == 0) return RAID6C_OK;
+  DeviceGuard g(plan->device);
+  ZP_CUDA(cudaMemsetAsync(bad_words, 0, static_cast<size_t>(num_stripes) * sizeof(uint32_t), plan->stream));
+  a.counts = bad_words;
+  return launch(plan, a, zp::KMODE_SCRUB, plan->stream);
+}
+
+raid6c_status raid6c_update_strided(raid6c_plan plan, uint8_t* data, size_t strip_stride, size_t stripe_stride,
+                                    uint8_t* P, uint8_t* Q, size_t parity_stride, int num_stripes,
+                                    const uint8_t* new_data, size_t new_stride, const int32_t* disks, int num_disks,
+                                    int disks_on_device) {
+  zp::ZpArgs a;
+  raid6c_status st = strided_args(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, a);
+  if (st != RAID6C_OK) return st;
+  if (!new_data || !disks) return RAID6C_E_NULL;
+  if (num_disks != 1 && num_disks != num_stripes) return RAID6C_E_SIZE;
+  if (num_stripes > 1 && new_stride < plan->bytes) return RAID6C_E_SIZE;
+  a.nbase = new_data;
+  a.new_stride = new_stride;
+  a.upd_rows = 4;
+  DeviceGuard g(plan->device);
+  if (disks_on_device) {
+    a.upd = disks;
+    a.upd_stride = num_disks == 1 ? 0 : 1;
+  } else if (num_disks == 1) {
+    if (disks[0] < 0 || disks[0] >= plan->N) return RAID6C_E_INVALID_INDEX;
+    a.upd_k = disks[0];
+  } else {
+    std::vector<raid6c_erasure> ev(num_disks);
+    for (int s = 0; s < num_disks; s++) {
+      if (disks[s] < 0 || disks[s] >= plan->N) return RAID6C_E_INVALID_INDEX;
+      ev[s] = {disks[s], plan->N};  // packed as (k, N): the kernel reads .x only
+    }
+    st = upload_erasures(plan, ev.data(), num_disks, plan->stream);
+    if (st != RAID6C_OK) return st;
+    a.upd = reinterpret_cast<const int32_t*>(plan->d_er);
+    a.upd_stride = 2;
+  }
+  return launch(plan, a, zp::KMODE_UPDATE, plan->stream);
 }
 
 raid6c_status raid6c_encode_host(raid6c_plan plan, const uint8_t* data, size_t strip_stride, size_t stripe_stride,

@@ -27,6 +27,15 @@ struct ZpArgs {
   //   tail: bytes [body_tiles*TB, pbytes) via direct loads, chunk_bytes per unit.
   uint64_t body_tiles;
   uint64_t tail_units_per_stripe;
+  // NEXT-1 modes.  update: strip upd[s*upd_stride] (or upd_k) of stripe s is rewritten with
+  // the new data at nbase + s*new_stride; scrub: counts[s] += words violating a parity equation.
+  const int32_t* upd;
+  int upd_rows;  // = 4 (old d_k, new d_k, P, Q); a runtime value on purpose, see num_rows()
+  int upd_stride;
+  int upd_k;
+  const uint8_t* nbase;
+  uint64_t new_stride;
+  uint32_t* counts;
 };
 
 // Kernel-geometry record for one compiled prime (fast path) -- filled by each
@@ -36,14 +45,14 @@ struct FastEntry {
   int chunk_bytes;  // bytes per thread-chunk (whole periods of lcm(n,32) bits)
   int tile_bytes;   // TMA row bytes = consumer threads * chunk_bytes
   int threads;      // consumer threads (+32 producer threads per CTA)
-  size_t smem_bytes;
-  const void* enc_kernel;  // __global__ void(ZpArgs)
-  const void* rec_kernel;
+  const void* kernel[4];  // __global__ void(ZpArgs) per mode: encode, recover, scrub, update
+  size_t smem_bytes[4];
 };
 
 const FastEntry* fast_entry(int p);  // nullptr if p has no fast path
 
 // Generic (runtime-p) kernels, any odd prime <= 257.
-cudaError_t generic_launch(const ZpArgs& a, int p, bool recover, cudaStream_t st, int num_sms);
+enum : int { KMODE_ENCODE = 0, KMODE_RECOVER = 1, KMODE_SCRUB = 2, KMODE_UPDATE = 3 };
+cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, int num_sms);
 
 }  // namespace zp

@@ -58,9 +58,6 @@ struct Geo {
   static constexpr int TB = THREADS * CB;            // TMA row (tile) bytes
   static constexpr int MTAB = (n + 1) * LAMBDA;      // mask table entries (uint2)
   static constexpr int SMEM_TARGET = 112 * 1024;     // 2 CTAs per SM
-  static constexpr int STAGES_RAW = (SMEM_TARGET - 2 * TB - MTAB * 8 - 256) / TB;
-  static constexpr int STAGES = STAGES_RAW < 3 ? 3 : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
-  static constexpr size_t SMEM = (size_t)(STAGES + 2) * TB + (size_t)MTAB * 8 + 2 * STAGES * 8;
   static_assert(LAMBDA <= 32, "fast path needs a period of at most 32 lanes");
   static_assert(TB % 16 == 0, "TMA rows must be multiples of 16 bytes");
 };
@@ -279,32 +276,57 @@ __device__ __forceinline__ void reduce(const Acc<G>& acc, uint32_t (&V)[G::C]) {
 }
 
 // ------------------------------------------------------------------ stripe bookkeeping
-enum : int { CLS_PQ = 0, CLS_DQ = 1, CLS_DP = 2, CLS_DD = 3 };
+enum : int { CLS_PQ = 0, CLS_DQ = 1, CLS_DP = 2, CLS_DD = 3, CLS_SCRUB = 4, CLS_UPDATE = 5 };
+// Kernel modes (compile-time): the method's two operations and the NEXT-1 pair around them.
+enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3 };
+constexpr int K_NEW = -1;  // row index of the update's new-data buffer
 
 struct ItemDesc {
-  int x, y;   // canonical lost pair, x < y
+  int x, y;   // canonical lost pair, x < y (update: x = the rewritten strip)
   int cls;    // CLS_*
   int base;   // rotation origin: amounts are (k - base) mod p
 };
 
-template <bool RECOVER>
+template <int MODE>
 __device__ __forceinline__ ItemDesc item_desc(const ZpArgs& a, int s) {
   ItemDesc d;
-  int i = a.N, j = a.N + 1;
-  if constexpr (RECOVER) {
-    if (a.er) {
-      const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
-      i = e.x; j = e.y;
-    } else {
-      i = a.ei; j = a.ej;
+  if constexpr (MODE == MODE_SCRUB) {
+    d.x = d.y = -1;
+    d.cls = CLS_SCRUB;
+    d.base = 0;
+    return d;
+  } else if constexpr (MODE == MODE_UPDATE) {
+    d.x = a.upd ? a.upd[static_cast<int64_t>(s) * a.upd_stride] : a.upd_k;
+    d.y = -1;
+    d.cls = CLS_UPDATE;
+    d.base = 0;
+    return d;
+  } else {
+    int i = a.N, j = a.N + 1;
+    if constexpr (MODE == MODE_RECOVER) {
+      if (a.er) {
+        const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
+        i = e.x; j = e.y;
+      } else {
+        i = a.ei; j = a.ej;
+      }
     }
+    d.x = i < j ? i : j;
+    d.y = i < j ? j : i;
+    if (d.y == a.N + 1) d.cls = (d.x == a.N) ? CLS_PQ : CLS_DQ;
+    else d.cls = (d.y == a.N) ? CLS_DP : CLS_DD;
+    d.base = (d.cls == CLS_DP || d.cls == CLS_DD) ? d.x : 0;
+    return d;
   }
-  d.x = i < j ? i : j;
-  d.y = i < j ? j : i;
-  if (d.y == a.N + 1) d.cls = (d.x == a.N) ? CLS_PQ : CLS_DQ;
-  else d.cls = (d.y == a.N) ? CLS_DP : CLS_DD;
-  d.base = (d.cls == CLS_DP || d.cls == CLS_DD) ? d.x : 0;
-  return d;
+}
+
+template <int MODE>
+__device__ __forceinline__ int num_rows(const ZpArgs& a) {
+  if constexpr (MODE == MODE_SCRUB) return a.N + 2;     // every strip of the stripe
+  // old d_k, new d_k, P, Q: the count (4) comes from the launch args so that the compiler keeps
+  // the row loop rolled (a compile-time 4 unrolls it and spills the accumulators)
+  else if constexpr (MODE == MODE_UPDATE) return a.upd_rows;
+  else return a.N;                                      // the N surviving strips
 }
 
 // r-th surviving strip (r in [0, N)), skipping the lost pair.
@@ -315,9 +337,22 @@ __device__ __forceinline__ int source_strip(int r, const ItemDesc& d) {
   return k;
 }
 
+// Strip index read by row r (K_NEW = the update's new-data buffer).
+template <int MODE>
+__device__ __forceinline__ int row_strip(const ZpArgs& a, int r, const ItemDesc& d) {
+  if constexpr (MODE == MODE_SCRUB) return r;
+  else if constexpr (MODE == MODE_UPDATE) return r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
+  else return source_strip(r, d);
+}
+
 __device__ __forceinline__ uint64_t strip_stride(const ZpArgs& a, int k) {
   return k < a.N ? a.data_stride : a.parity_stride;
 }
+__device__ __forceinline__ const uint8_t* row_ptr(const ZpArgs& a, int k, int s) {
+  return k == K_NEW ? a.nbase + static_cast<uint64_t>(s) * a.new_stride
+                    : a.base[k] + static_cast<uint64_t>(s) * strip_stride(a, k);
+}
+__device__ __forceinline__ uint64_t row_len(const ZpArgs& a, int k) { return k < a.N ? a.bytes : a.pbytes; }
 
 // Fold one source row into the accumulators (P part and rotated Q part).
 template <class G>
@@ -333,6 +368,27 @@ __device__ __forceinline__ void fold_row(const ZpArgs& a, const ItemDesc& d, int
     if (amt < 0) amt += G::P;
     rot_acc<G>(L, amt, mtab, acc);
   }
+}
+
+// Number of words of a chunk with a nonzero bit in V (compile-time word layout).
+template <class G>
+__device__ __forceinline__ uint32_t count_nonzero_words(const uint32_t (&V)[G::C]) {
+  constexpr int WORDS = 32 * G::C / G::n;
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int w = 0; w < WORDS; w++) {
+    const int b0 = w * G::n, b1 = b0 + G::n;
+    uint32_t any = 0;
+#pragma unroll
+    for (int l = b0 / 32; l <= (b1 - 1) / 32; l++) {
+      const int lo = b0 > 32 * l ? b0 - 32 * l : 0;
+      const int hi = b1 < 32 * l + 32 ? b1 - 32 * l : 32;
+      const uint32_t m = (hi - lo == 32) ? 0xFFFFFFFFu : (((1u << (hi - lo)) - 1u) << lo);
+      any |= V[l] & m;
+    }
+    cnt += any != 0u;
+  }
+  return cnt;
 }
 
 // Class epilogue: produces the two output chunks and their strip indices.
@@ -393,14 +449,60 @@ __device__ __forceinline__ void finish(const ZpArgs& a, const ItemDesc& d, uint3
 }
 
 // ------------------------------------------------------------------ the kernel
-template <int P, bool RECOVER>
+template <int MODE>
+__host__ __device__ constexpr int num_outputs() {
+  return MODE == MODE_SCRUB ? 0 : (MODE == MODE_UPDATE ? 3 : 2);
+}
+
+// Shared-memory layout per (p, mode): STAGES TMA rows, NOUT output rows, mask table, barriers.
+template <int P, int MODE>
+struct Layout {
+  using G = Geo<P>;
+  static constexpr int NOUT = num_outputs<MODE>();
+  static constexpr int STAGES_RAW = (G::SMEM_TARGET - NOUT * G::TB - G::MTAB * 8 - 256) / G::TB;
+  static constexpr int STAGES = STAGES_RAW < 3 ? 3 : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
+  static constexpr size_t SMEM = (size_t)(STAGES + NOUT) * G::TB + (size_t)G::MTAB * 8 + 2 * STAGES * 8;
+};
+
+// Per-item epilogue for every mode: fills the NOUT output chunks and their strip indices
+// (scrub: adds the count of words violating a parity equation to a.counts[s]).
+template <int MODE, class G, bool WARP_UNIFORM = true>
+__device__ __forceinline__ void epilogue(const ZpArgs& a, const ItemDesc& d, int s, uint32_t (&Pa)[G::C], Acc<G>& acc,
+                                         const uint32_t (&NEW)[G::C], const uint2* __restrict__ mtab,
+                                         uint32_t (&o0)[G::C], uint32_t (&o1)[G::C], int& k0, int& k1, int& k2) {
+  constexpr int C = G::C;
+  if constexpr (MODE == MODE_SCRUB) {
+    // syndromes of both parity equations (Eq. (znparity)): S_P = P + sum d_i, S_Q = Q + sum x^i d_i
+    reduce<G>(acc, o1);
+#pragma unroll
+    for (int l = 0; l < C; l++) o1[l] |= Pa[l];
+    uint32_t bad = count_nonzero_words<G>(o1);
+    if constexpr (WARP_UNIFORM) {  // body items: the whole warp works on stripe s
+      bad = __reduce_add_sync(0xffffffffu, bad);
+      if ((threadIdx.x & 31) == 0 && bad) atomicAdd(a.counts + s, bad);
+    } else if (bad) {
+      atomicAdd(a.counts + s, bad);
+    }
+  } else if constexpr (MODE == MODE_UPDATE) {
+    // P' = P + (old + new), Q' = Q + x^k (old + new)  (linearity of Eq. (znparity)); d_k' = new
+#pragma unroll
+    for (int l = 0; l < C; l++) o0[l] = Pa[l];
+    reduce<G>(acc, o1);
+    k0 = a.N; k1 = a.N + 1; k2 = d.x;
+  } else {
+    finish<G>(a, d, Pa, acc, mtab, o0, o1, k0, k1);
+  }
+}
+
+template <int P, int MODE>
 __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __grid_constant__ ZpArgs a) {
   using G = Geo<P>;
-  constexpr int C = G::C, CB = G::CB, TB = G::TB, NT = G::THREADS, ST = G::STAGES;
+  using LY = Layout<P, MODE>;
+  constexpr int C = G::C, CB = G::CB, TB = G::TB, NT = G::THREADS, ST = LY::STAGES, NOUT = LY::NOUT;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint8_t* outb = smem + (size_t)ST * TB;
-  uint2* mtab = reinterpret_cast<uint2*>(outb + 2 * TB);
+  uint2* mtab = reinterpret_cast<uint2*>(outb + (size_t)NOUT * TB);
   uint64_t* full = reinterpret_cast<uint64_t*>(mtab + G::MTAB);
   uint64_t* empty = full + ST;
 
@@ -430,6 +532,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
 
   const uint64_t tiles = a.body_tiles;
   const uint64_t body_items = tiles * static_cast<uint64_t>(a.num_stripes);
+  const int R = num_rows<MODE>(a);
 
   if (warp == NT / 32) {
     // ------------------------------------------------ producer: one lane issues all TMA rows
@@ -438,10 +541,9 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
       for (uint64_t it = blockIdx.x; it < body_items; it += gridDim.x) {
         const int s = static_cast<int>(it / tiles);
         const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
-        const ItemDesc d = item_desc<RECOVER>(a, s);
-        for (int r = 0; r < a.N; r++) {
-          const int k = source_strip(r, d);
-          const uint8_t* g = a.base[k] + static_cast<uint64_t>(s) * strip_stride(a, k) + t * TB;
+        const ItemDesc d = item_desc<MODE>(a, s);
+        for (int r = 0; r < R; r++) {
+          const uint8_t* g = row_ptr(a, row_strip<MODE>(a, r, d), s) + t * TB;
           mbar_wait(&empty[stage], ph ^ 1u);
           mbar_expect_tx(&full[stage], TB);
           tma_load_row(stages + (size_t)stage * TB, g, TB, &full[stage]);
@@ -457,17 +559,28 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
   for (uint64_t it = blockIdx.x; it < body_items; it += gridDim.x) {
     const int s = static_cast<int>(it / tiles);
     const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
-    const ItemDesc d = item_desc<RECOVER>(a, s);
+    const ItemDesc d = item_desc<MODE>(a, s);
     uint32_t Pa[C];
+    uint32_t NEW[C];  // unused in the body path (update stages the new row in SMEM)
     Acc<G> acc;
     acc.zero();
 #pragma unroll
     for (int l = 0; l < C; l++) Pa[l] = 0;
-    for (int r = 0; r < a.N; r++) {
-      const int k = source_strip(r, d);
+    if constexpr (MODE == MODE_UPDATE) {  // the new row goes straight to output slot 2
+      if (tid == 0) bulk_wait_read0();
+      named_bar_sync(1, NT);
+    }
+    for (int r = 0; r < R; r++) {
+      int k = row_strip<MODE>(a, r, d);
       uint32_t L[C];
       mbar_wait(&full[stage], ph);
       ld_chunk_smem<C>(stages + (size_t)stage * TB + tid * CB, L);
+      if constexpr (MODE == MODE_UPDATE) {
+        if (k == K_NEW) {
+          k = d.x;  // the new data folds in like the strip it replaces
+          st_chunk_smem<C>(outb + 2 * TB + tid * CB, L);
+        }
+      }
       fold_row<G>(a, d, k, L, mtab, Pa, acc);
       // Release the stage only after every loaded lane has been consumed: an mbarrier.arrive
       // issued right after the LDS does not wait for the loads to complete, and the producer's
@@ -477,19 +590,23 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
       if (++stage == ST) { stage = 0; ph ^= 1u; }
     }
     uint32_t o0[C], o1[C];
-    int k0, k1;
-    finish<G>(a, d, Pa, acc, mtab, o0, o1, k0, k1);
-    if (tid == 0) bulk_wait_read0();  // previous item's bulk stores have read outb
-    named_bar_sync(1, NT);
-    st_chunk_smem<C>(outb + tid * CB, o0);
-    st_chunk_smem<C>(outb + TB + tid * CB, o1);
-    fence_proxy_async_smem();
-    named_bar_sync(1, NT);
-    if (tid == 0) {
-      tma_store_row(const_cast<uint8_t*>(a.base[k0]) + static_cast<uint64_t>(s) * strip_stride(a, k0) + t * TB, outb, TB);
-      tma_store_row(const_cast<uint8_t*>(a.base[k1]) + static_cast<uint64_t>(s) * strip_stride(a, k1) + t * TB,
-                    outb + TB, TB);
-      bulk_commit();
+    int k0 = 0, k1 = 0, k2 = 0;
+    epilogue<MODE, G>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+    if constexpr (NOUT > 0) {
+      if constexpr (MODE != MODE_UPDATE) {  // (update waited at the start of the item)
+        if (tid == 0) bulk_wait_read0();  // previous item's bulk stores have read outb
+        named_bar_sync(1, NT);
+      }
+      st_chunk_smem<C>(outb + tid * CB, o0);
+      st_chunk_smem<C>(outb + TB + tid * CB, o1);
+      fence_proxy_async_smem();
+      named_bar_sync(1, NT);
+      if (tid == 0) {
+        tma_store_row(const_cast<uint8_t*>(row_ptr(a, k0, s)) + t * TB, outb, TB);
+        tma_store_row(const_cast<uint8_t*>(row_ptr(a, k1, s)) + t * TB, outb + TB, TB);
+        if constexpr (NOUT == 3) tma_store_row(const_cast<uint8_t*>(row_ptr(a, k2, s)) + t * TB, outb + 2 * TB, TB);
+        bulk_commit();
+      }
     }
   }
 
@@ -501,28 +618,38 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
        u += static_cast<uint64_t>(gridDim.x) * NT) {
     const int s = static_cast<int>(u / tups);
     const uint64_t off = body_end + (u - static_cast<uint64_t>(s) * tups) * CB;
-    const ItemDesc d = item_desc<RECOVER>(a, s);
+    const ItemDesc d = item_desc<MODE>(a, s);
     uint32_t Pa[C];
+    uint32_t NEW[C];  // update mode only (dead otherwise)
     Acc<G> acc;
     acc.zero();
 #pragma unroll
     for (int l = 0; l < C; l++) Pa[l] = 0;
-    for (int r = 0; r < a.N; r++) {
-      const int k = source_strip(r, d);
-      const uint64_t len = k < a.N ? a.bytes : a.pbytes;
+#pragma unroll 1
+    for (int r = 0; r < R; r++) {
+      int k = row_strip<MODE>(a, r, d);
       uint32_t L[C];
-      ld_chunk_global<C>(a.base[k] + static_cast<uint64_t>(s) * strip_stride(a, k) + off, off, len, L);
+      ld_chunk_global<C>(row_ptr(a, k, s) + off, off, row_len(a, k), L);
+      if constexpr (MODE == MODE_UPDATE) {
+        if (k == K_NEW) {  // old d_k (row 0) of this chunk is already folded: overwrite it now
+          k = d.x;
+          st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k, s)) + off, off, row_len(a, k), L);
+        }
+      }
       fold_row<G>(a, d, k, L, mtab, Pa, acc);
     }
     uint32_t o0[C], o1[C];
-    int k0, k1;
-    finish<G>(a, d, Pa, acc, mtab, o0, o1, k0, k1);
-    st_chunk_global<C>(const_cast<uint8_t*>(a.base[k0]) + static_cast<uint64_t>(s) * strip_stride(a, k0) + off, off,
-                       k0 < a.N ? a.bytes : a.pbytes, o0);
-    st_chunk_global<C>(const_cast<uint8_t*>(a.base[k1]) + static_cast<uint64_t>(s) * strip_stride(a, k1) + off, off,
-                       k1 < a.N ? a.bytes : a.pbytes, o1);
+    int k0 = 0, k1 = 0, k2 = 0;
+    if constexpr (MODE == MODE_SCRUB) {  // lanes of a warp may work on different stripes here
+      epilogue<MODE, G, false>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+    } else {
+      epilogue<MODE, G>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+      st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k0, s)) + off, off, row_len(a, k0), o0);
+      st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k1, s)) + off, off, row_len(a, k1), o1);
+    }
   }
-  if (tid == 0) bulk_wait0();
+  if constexpr (NOUT > 0)
+    if (tid == 0) bulk_wait0();
 }
 
 template <int P>
@@ -533,20 +660,27 @@ FastEntry make_entry() {
   e.chunk_bytes = G::CB;
   e.tile_bytes = G::TB;
   e.threads = G::THREADS;
-  e.smem_bytes = G::SMEM;
-  e.enc_kernel = reinterpret_cast<const void*>(&zp_kernel<P, false>);
-  e.rec_kernel = reinterpret_cast<const void*>(&zp_kernel<P, true>);
+  e.kernel[MODE_ENCODE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_ENCODE>);
+  e.kernel[MODE_RECOVER] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_RECOVER>);
+  e.kernel[MODE_SCRUB] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_SCRUB>);
+  e.kernel[MODE_UPDATE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_UPDATE>);
+  e.smem_bytes[MODE_ENCODE] = Layout<P, MODE_ENCODE>::SMEM;
+  e.smem_bytes[MODE_RECOVER] = Layout<P, MODE_RECOVER>::SMEM;
+  e.smem_bytes[MODE_SCRUB] = Layout<P, MODE_SCRUB>::SMEM;
+  e.smem_bytes[MODE_UPDATE] = Layout<P, MODE_UPDATE>::SMEM;
   return e;
 }
 
 }  // namespace zp
 
-#define ZP_INSTANTIATE_FAST(PP)                                                   \
-  namespace zp {                                                                  \
-  template __global__ void zp_kernel<PP, false>(const __grid_constant__ ZpArgs); \
-  template __global__ void zp_kernel<PP, true>(const __grid_constant__ ZpArgs);  \
-  const FastEntry* fast_entry_##PP() {                                            \
-    static const FastEntry e = make_entry<PP>();                                  \
-    return &e;                                                                    \
-  }                                                                               \
+#define ZP_INSTANTIATE_FAST(PP)                                                        \
+  namespace zp {                                                                       \
+  template __global__ void zp_kernel<PP, MODE_ENCODE>(const __grid_constant__ ZpArgs);  \
+  template __global__ void zp_kernel<PP, MODE_RECOVER>(const __grid_constant__ ZpArgs); \
+  template __global__ void zp_kernel<PP, MODE_SCRUB>(const __grid_constant__ ZpArgs);   \
+  template __global__ void zp_kernel<PP, MODE_UPDATE>(const __grid_constant__ ZpArgs);  \
+  const FastEntry* fast_entry_##PP() {                                                 \
+    static const FastEntry e = make_entry<PP>();                                       \
+    return &e;                                                                         \
+  }                                                                                    \
   }

@@ -68,12 +68,22 @@ __device__ void reduce(Word& w, int p) {
 }
 
 struct Desc {
-  int x, y, cls, base;
+  int x, y, cls, base;  // cls: 0 PQ, 1 DQ, 2 DP, 3 DD, 4 scrub, 5 update (x = rewritten strip)
 };
 
-__device__ Desc desc_of(const ZpArgs& a, int s, bool recover) {
+__device__ Desc desc_of(const ZpArgs& a, int s, int mode) {
+  Desc d;
+  if (mode == KMODE_SCRUB) {
+    d.x = d.y = -1; d.cls = 4; d.base = 0;
+    return d;
+  }
+  if (mode == KMODE_UPDATE) {
+    d.x = a.upd ? a.upd[static_cast<int64_t>(s) * a.upd_stride] : a.upd_k;
+    d.y = -1; d.cls = 5; d.base = 0;
+    return d;
+  }
   int i = a.N, j = a.N + 1;
-  if (recover) {
+  if (mode == KMODE_RECOVER) {
     if (a.er) {
       const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
       i = e.x; j = e.y;
@@ -81,49 +91,68 @@ __device__ Desc desc_of(const ZpArgs& a, int s, bool recover) {
       i = a.ei; j = a.ej;
     }
   }
-  Desc d;
   d.x = i < j ? i : j;
   d.y = i < j ? j : i;
   if (d.y == a.N + 1) d.cls = (d.x == a.N) ? 0 : 1;  // PQ : DQ
   else d.cls = (d.y == a.N) ? 2 : 3;                  // DP : DD
-  d.base = (d.cls >= 2) ? d.x : 0;
+  d.base = (d.cls == 2 || d.cls == 3) ? d.x : 0;
   return d;
 }
 
 __device__ __forceinline__ uint64_t sstride(const ZpArgs& a, int k) { return k < a.N ? a.data_stride : a.parity_stride; }
+constexpr int K_NEW = -1;
+__device__ __forceinline__ const uint8_t* rptr(const ZpArgs& a, int k, int s) {
+  return k == K_NEW ? a.nbase + static_cast<uint64_t>(s) * a.new_stride : a.base[k] + static_cast<uint64_t>(s) * sstride(a, k);
+}
+__device__ __forceinline__ uint64_t rlen(const ZpArgs& a, int k) { return k < a.N ? a.bytes : a.pbytes; }
 
 constexpr int GROUP_MAX_BYTES = 128;  // g*n/8 <= n/2 <= 128
 
-__global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int recover) {
+__global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int mode) {
   const int n = p - 1;
   const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);  // 8 / gcd(n, 8)
   const int gbytes = g * n / 8;
   const uint64_t W = (8 * a.bytes + n - 1) / n;
   const uint64_t groups = (W + g - 1) / g;
   const uint64_t total = groups * static_cast<uint64_t>(a.num_stripes);
+  const int R = mode == KMODE_SCRUB ? a.N + 2 : (mode == KMODE_UPDATE ? a.upd_rows : a.N);
   for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
        u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int s = static_cast<int>(u / groups);
     const uint64_t grp = u - static_cast<uint64_t>(s) * groups;
-    const Desc d = desc_of(a, s, recover != 0);
-    int k0, k1;
-    if (d.cls == 0) { k0 = a.N; k1 = a.N + 1; }
-    else if (d.cls == 1) { k0 = d.x; k1 = a.N + 1; }
-    else if (d.cls == 2) { k0 = d.x; k1 = a.N; }
-    else { k0 = d.x; k1 = d.y; }
-    uint8_t ob0[GROUP_MAX_BYTES], ob1[GROUP_MAX_BYTES];
-    for (int i = 0; i < gbytes; i++) { ob0[i] = 0; ob1[i] = 0; }
+    const Desc d = desc_of(a, s, mode);
+    int kout[3] = {0, 0, 0};
+    int nout = 2;
+    if (d.cls == 0) { kout[0] = a.N; kout[1] = a.N + 1; }
+    else if (d.cls == 1) { kout[0] = d.x; kout[1] = a.N + 1; }
+    else if (d.cls == 2) { kout[0] = d.x; kout[1] = a.N; }
+    else if (d.cls == 3) { kout[0] = d.x; kout[1] = d.y; }
+    else if (d.cls == 4) { nout = 0; }
+    else { kout[0] = a.N; kout[1] = a.N + 1; kout[2] = d.x; nout = 3; }
+    uint8_t ob[3][GROUP_MAX_BYTES];
+    for (int q = 0; q < 3; q++)
+      for (int i = 0; i < gbytes; i++) ob[q][i] = 0;
+    uint32_t bad = 0;
     for (int wi = 0; wi < g; wi++) {
       const uint64_t w = grp * g + wi;
-      Word Pa, acc, L, o0, o1;
+      Word Pa, acc, L, NEWW, o[3];
       wzero(Pa);
       wzero(acc);
-      for (int r = 0; r < a.N; r++) {
-        int k = r;
-        if (k >= d.x) k++;
-        if (k >= d.y) k++;
-        const uint64_t len = k < a.N ? a.bytes : a.pbytes;
-        load_word(a.base[k] + static_cast<uint64_t>(s) * sstride(a, k), len, w, n, L);
+      wzero(NEWW);
+      for (int r = 0; r < R; r++) {
+        int k;
+        if (mode == KMODE_SCRUB) k = r;
+        else if (mode == KMODE_UPDATE) k = r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
+        else {
+          k = r;
+          if (k >= d.x) k++;
+          if (k >= d.y) k++;
+        }
+        load_word(rptr(a, k, s), rlen(a, k), w, n, L);
+        if (k == K_NEW) {
+          NEWW = L;
+          k = d.x;
+        }
         if (k <= a.N) wxor(Pa, L);
         if (k != a.N) {
           int amt = ((k < a.N ? k : p) - d.base) % p;
@@ -132,20 +161,20 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int r
         }
       }
       if (d.cls == 0) {
-        o0 = Pa;
+        o[0] = Pa;
         reduce(acc, p);
-        o1 = acc;
+        o[1] = acc;
       } else if (d.cls == 1) {
-        o0 = Pa;
+        o[0] = Pa;
         rot_acc(acc, Pa, d.x, p);
         reduce(acc, p);
-        o1 = acc;
+        o[1] = acc;
       } else if (d.cls == 2) {
         reduce(acc, p);
-        o0 = acc;
-        o1 = Pa;
-        wxor(o1, o0);
-      } else {
+        o[0] = acc;
+        o[1] = Pa;
+        wxor(o[1], o[0]);
+      } else if (d.cls == 3) {
         wxor(acc, Pa);
         reduce(acc, p);
         const Word t = acc;
@@ -168,30 +197,45 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int r
             m += 1;
           }
         }
-        o1 = S;
-        o0 = S;
-        wxor(o0, Pa);
+        o[1] = S;
+        o[0] = S;
+        wxor(o[0], Pa);
+      } else if (d.cls == 4) {  // scrub: syndromes of both parity equations
+        reduce(acc, p);
+        wxor(acc, Pa);
+        int nz = 0;
+        for (int j = 0; j < NL; j++) nz |= acc.v[j] != 0;
+        for (int j = 0; j < NL; j++) nz |= Pa.v[j] != 0;
+        bad += (w < W) && nz;
+      } else {  // update
+        o[0] = Pa;
+        reduce(acc, p);
+        o[1] = acc;
+        o[2] = NEWW;
       }
-      for (int j = 0; j < n; j++) {
-        const int bpos = wi * n + j;
-        ob0[bpos >> 3] |= static_cast<uint8_t>(wbit(o0, j) << (bpos & 7));
-        ob1[bpos >> 3] |= static_cast<uint8_t>(wbit(o1, j) << (bpos & 7));
-      }
+      for (int q = 0; q < nout; q++)
+        for (int j = 0; j < n; j++) {
+          const int bpos = wi * n + j;
+          ob[q][bpos >> 3] |= static_cast<uint8_t>(wbit(o[q], j) << (bpos & 7));
+        }
+    }
+    if (mode == KMODE_SCRUB) {
+      if (bad) atomicAdd(a.counts + s, bad);
+      continue;
     }
     const uint64_t byte0 = grp * static_cast<uint64_t>(gbytes);
-    uint8_t* g0 = const_cast<uint8_t*>(a.base[k0]) + static_cast<uint64_t>(s) * sstride(a, k0);
-    uint8_t* g1 = const_cast<uint8_t*>(a.base[k1]) + static_cast<uint64_t>(s) * sstride(a, k1);
-    const uint64_t len0 = k0 < a.N ? a.bytes : a.pbytes, len1 = k1 < a.N ? a.bytes : a.pbytes;
-    for (int i = 0; i < gbytes; i++) {
-      if (byte0 + i < len0) g0[byte0 + i] = ob0[i];
-      if (byte0 + i < len1) g1[byte0 + i] = ob1[i];
+    for (int q = 0; q < nout; q++) {
+      uint8_t* gq = const_cast<uint8_t*>(rptr(a, kout[q], s));
+      const uint64_t len = rlen(a, kout[q]);
+      for (int i = 0; i < gbytes; i++)
+        if (byte0 + i < len) gq[byte0 + i] = ob[q][i];
     }
   }
 }
 
 }  // namespace
 
-cudaError_t generic_launch(const ZpArgs& a, int p, bool recover, cudaStream_t st, int num_sms) {
+cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, int num_sms) {
   const int n = p - 1;
   const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);
   const uint64_t W = (8 * a.bytes + n - 1) / n;
@@ -201,7 +245,7 @@ cudaError_t generic_launch(const ZpArgs& a, int p, bool recover, cudaStream_t st
   const uint64_t cap = static_cast<uint64_t>(num_sms) * 16;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
-  zp_generic_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(a, p, recover ? 1 : 0);
+  zp_generic_kernel<<<static_cast<unsigned>(blocks), threads, 0, st>>>(a, p, mode);
   return cudaGetLastError();
 }
 

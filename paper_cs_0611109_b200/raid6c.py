@@ -49,6 +49,8 @@ _SIGS = [
     ("raid6c_recover", _i, [_i, _i, _i, _i, ctypes.POINTER(_vp), _sz]),
     ("raid6c_encode_strided", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i]),
     ("raid6c_recover_strided", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _i, _i]),
+    ("raid6c_scrub_strided", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp]),
+    ("raid6c_update_strided", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _sz, _vp, _i, _i]),
     ("raid6c_encode_host", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i]),
     ("raid6c_recover_host", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _i]),
     ("raid6c_host_traffic", _i, [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
@@ -197,6 +199,24 @@ class Plan:
             _check(_lib.raid6c_recover_strided(self._h, _ptr(data), strip_stride, stripe_stride, _ptr(P), _ptr(Q),
                                                parity_stride, num_stripes, ctypes.cast(arr, _vp), len(arr), 0),
                    "raid6c_recover_strided")
+
+    def scrub_strided(self, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, bad_words):
+        """bad_words: uint32 (or int32) CUDA tensor [num_stripes], overwritten with per-stripe counts."""
+        _check(_lib.raid6c_scrub_strided(self._h, _ptr(data), strip_stride, stripe_stride, _ptr(P), _ptr(Q),
+                                         parity_stride, num_stripes, _ptr(bad_words)), "raid6c_scrub_strided")
+
+    def update_strided(self, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, new_data,
+                       new_stride, disks):
+        """disks: list of strip indices (1 or num_stripes) or an int32 CUDA tensor [S]."""
+        if hasattr(disks, "is_cuda") and disks.is_cuda:
+            _check(_lib.raid6c_update_strided(self._h, _ptr(data), strip_stride, stripe_stride, _ptr(P), _ptr(Q),
+                                              parity_stride, num_stripes, _ptr(new_data), new_stride, _ptr(disks),
+                                              disks.shape[0], 1), "raid6c_update_strided")
+        else:
+            arr = (ctypes.c_int32 * len(disks))(*[int(k) for k in disks])
+            _check(_lib.raid6c_update_strided(self._h, _ptr(data), strip_stride, stripe_stride, _ptr(P), _ptr(Q),
+                                              parity_stride, num_stripes, _ptr(new_data), new_stride,
+                                              ctypes.cast(arr, _vp), len(arr), 0), "raid6c_update_strided")
 
     def encode_host(self, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes):
         _check(_lib.raid6c_encode_host(self._h, _ptr(data), strip_stride, stripe_stride, _ptr(P), _ptr(Q),
