@@ -278,7 +278,7 @@ def run_ours(args):
         "verified": verified, "e2e": e2e,
         "fast_path": R.has_fast_path(p),
     }
-    if rank == 0 and args.cpu_baseline:
+    if rank == 0 and world == 1 and args.cpu_baseline:  # the oracle baseline: rank 0 at N=1 only
         line["cpu_baseline"] = cpu_baseline(args, p, N, nbytes, args.config, c["sparse"])
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -286,6 +286,76 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_next1(args):
+    """--op update | scrub (NEXT-1): small-write parity update and scrub of the
+    config's stripes, one launch per step, CUDA events on the plan's stream."""
+    import torch
+    from paper_cs_0611109_b200 import raid6c as R
+
+    rank, world, local = _env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    c = CONFIGS[args.config]
+    p, N, S = c["p"], c["N"], args.stripes or c["stripes"]
+    nbytes = args.strip_bytes or c["nbytes"]
+    pb = R.parity_bytes(p, nbytes)
+    ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
+    stream = torch.cuda.Stream(device=dev)
+    data = torch.empty((S, N, ss), dtype=torch.uint8, device=dev)
+    par = torch.zeros((S, 2, ps), dtype=torch.uint8, device=dev)
+    R.fill(data, ss, N * ss, nbytes, N, S, 0, args.config, 0, 0, c["sparse"], stream)
+    news = [torch.empty((S, ss), dtype=torch.uint8, device=dev) for _ in range(2)]
+    for i, nb in enumerate(news):
+        R.fill(nb, ss, ss, nbytes, 1, S, 1 + i, args.config, 0, 0, 0, stream)
+    plan = R.Plan(p, N, nbytes, local, stream)
+    a = (int(data.data_ptr()), ss, N * ss, int(par.data_ptr()), int(par.data_ptr()) + ps, 2 * ps, S)
+    plan.encode_strided(*a)
+    disks = torch.tensor([(7 * s) % N for s in range(S)], dtype=torch.int32, device=dev)
+    counts = torch.zeros(S, dtype=torch.int32, device=dev)
+
+    def launch(t):
+        if args.op == "update":
+            plan.update_strided(*a, int(news[t % 2].data_ptr()), ss, disks)
+        else:
+            plan.scrub_strided(*a, counts)
+
+    total = args.warmup + args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(total)]
+    torch.cuda.synchronize(dev)
+    launches0 = R.launch_count()
+    for t in range(total):
+        with torch.cuda.stream(stream):
+            evs[t][0].record(stream)
+            launch(t)
+            evs[t][1].record(stream)
+    stream.synchronize()
+    launches = R.launch_count() - launches0 - args.warmup
+    ms = statistics.mean(evs[t][0].elapsed_time(evs[t][1]) for t in range(args.warmup, total))
+    plan.scrub_strided(*a, counts)  # verification: every stripe consistent after the updates
+    stream.synchronize()
+    bad = int(counts.sum().item())
+    if args.op == "update":
+        alg = S * (3 * nbytes + 4 * pb)
+        user = S * nbytes
+        metric = "small-write parity update (NEXT-1) GB/s of rewritten user data"
+    else:
+        alg = S * (N * nbytes + 2 * pb)
+        user = S * N * nbytes
+        metric = "scrub (NEXT-1) GB/s of user data checked"
+    peak, peak_src = measured_peak()
+    ach = alg / (ms / 1e3) / 1e9
+    line = {"metric": metric, "value": round(user / (ms / 1e3) / 1e9, 2), "unit": "GB/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+            "op": args.op, "dtype": "u32 (bitwise GF(2) words)", "data": "synthetic (device generator)",
+            "config": {"workload": c["desc"], "p": p, "N": N, "strip_bytes": nbytes, "stripes": S},
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "peak_source": peak_src, "alg_bytes_per_launch": alg},
+            "gpu_launches": launches, "verified": {"scrub_bad_words_after": bad}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
 
 
 def run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_lists, do_rec, world, dev):
@@ -441,6 +511,8 @@ def main():
     ap.add_argument("--stripes", type=int, default=0, help="override stripes per GPU per step")
     ap.add_argument("--strip-bytes", type=int, default=0, help="override strip length (c3 sweep)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--op", default="step", choices=["step", "update", "scrub"],
+                    help="step = encode + recover (the metric); update / scrub = NEXT-1 kernels")
     ap.add_argument("--no-verify", dest="verify", action="store_false")
     ap.add_argument("--no-oracle-check", dest="oracle_check", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
@@ -454,6 +526,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.op != "step":
+        run_next1(args)
     else:
         run_ours(args)
 
