@@ -65,6 +65,10 @@ def _lib():
             lib.oracle_recover.argtypes = [i, i, i, i, pp, sz]
             lib.oracle_count_bad_words.argtypes = [i, i, pp, sz]
             lib.oracle_count_bad_words.restype = sz
+            lib.oracle_ext_condition.argtypes = [i]
+            lib.oracle_ext_coeff.argtypes = [i, i, u8p]
+            lib.oracle_encode_ext.argtypes = [i, i, pp, sz, u8p, u8p]
+            lib.oracle_recover_ext.argtypes = [i, i, i, i, pp, sz]
             _lib_handle = lib
     return _lib_handle
 
@@ -200,3 +204,38 @@ def recover(p: int, N: int, lost_i: int, lost_j: int, strips, nbytes: int):
 
 def count_bad_words(p: int, N: int, strips, nbytes: int) -> int:
     return int(_lib().oracle_count_bad_words(p, N, _ptr_array(strips), nbytes))
+
+
+# ------------------------------------------------------ extended Q-parity (NEXT-2)
+def ext_condition(p: int) -> bool:
+    """Theorem 25.3(3): gcd(X^p + 1, X^m + X + 1) = 1 for all 0 < m < p."""
+    return bool(_lib().oracle_ext_condition(p))
+
+
+def ext_coeff(p: int, k: int) -> np.ndarray:
+    n = p - 1
+    G = np.zeros((n, n), np.uint8)
+    _lib().oracle_ext_coeff(p, k, _p(G))
+    return G
+
+
+def encode_ext(p: int, data, nbytes: int | None = None):
+    """Eq. (qext): D = len(data) data strips, 1 <= D <= 2p-1."""
+    if nbytes is None:
+        nbytes = int(np.asarray(data[0]).size)
+    data = _as_strips(data, nbytes)
+    pb = parity_bytes(p, nbytes)
+    P = np.zeros(pb, np.uint8)
+    Q = np.zeros(pb, np.uint8)
+    rc = _lib().oracle_encode_ext(p, len(data), _ptr_array(data), nbytes, _p(P), _p(Q))
+    if rc != 0:
+        raise ValueError(f"oracle_encode_ext: invalid arguments p={p} D={len(data)}")
+    return P, Q
+
+
+def recover_ext(p: int, D: int, lost_i: int, lost_j: int, strips, nbytes: int):
+    assert len(strips) == D + 2
+    rc = _lib().oracle_recover_ext(p, D, lost_i, lost_j, _ptr_array(strips), nbytes)
+    if rc != 0:
+        raise ValueError(f"oracle_recover_ext failed rc={rc} (p={p} D={D} lost=({lost_i},{lost_j}))")
+    return strips

@@ -378,13 +378,18 @@ int oracle_recover(int p, int N, int lost_i, int lost_j, uint8_t *const *strips,
  * Syndrome check of a complete stripe (both parity equations of Eq. (znparity)):
  * returns the number of words w for which P_w != sum d or Q_w != sum g^i d.
  */
+int oracle_encode_ext(int p, int D, const uint8_t *const *strips, size_t bytes, uint8_t *P, uint8_t *Q);
+
 size_t oracle_count_bad_words(int p, int N, const uint8_t *const *strips, size_t bytes) {
-    if (!oracle_valid_p(p) || N < 1 || N > p) return (size_t)-1;
+    if (!oracle_valid_p(p) || N < 1 || N > 2 * p - 1) return (size_t)-1;
     int n = p - 1;
+    if (n < 1 || n > ORACLE_MAX_N) return (size_t)-1;
     size_t W = oracle_word_count(p, bytes);
     size_t pb = oracle_parity_bytes(p, bytes);
     uint8_t *Pc = (uint8_t *)malloc(pb), *Qc = (uint8_t *)malloc(pb);
-    oracle_encode(p, N, strips, bytes, Pc, Qc);
+    /* the parity equations: Eq. (znparity) for N <= p, Eq. (qext) beyond (NEXT-2) */
+    if (N <= p) oracle_encode(p, N, strips, bytes, Pc, Qc);
+    else if (oracle_encode_ext(p, N, strips, bytes, Pc, Qc) != 0) { free(Pc); free(Qc); return (size_t)-1; }
     uint8_t a[ORACLE_MAX_N], b[ORACLE_MAX_N];
     size_t bad = 0;
     for (size_t w = 0; w < W; w++) {
@@ -397,4 +402,203 @@ size_t oracle_count_bad_words(int p, int N, const uint8_t *const *strips, size_t
     }
     free(Pc); free(Qc);
     return bad;
+}
+
+/* =====================================================================================
+ * Extended Q-parity (NEXT-2): Sec. 3.3, Theorem 25.3 and Eq. (qext).
+ * ===================================================================================== */
+
+/* Polynomials over F2 as coefficient arrays (one byte per coefficient), degree tracked. */
+static int poly_deg(const uint8_t *a, int len) {
+    for (int i = len - 1; i >= 0; i--)
+        if (a[i]) return i;
+    return -1;
+}
+
+/* gcd(a, b) over F2 by Euclid's algorithm with plain long division; returns its degree. */
+static int poly_gcd_deg(const uint8_t *a0, const uint8_t *b0, int len) {
+    uint8_t *a = (uint8_t *)malloc((size_t)len), *b = (uint8_t *)malloc((size_t)len);
+    memcpy(a, a0, (size_t)len);
+    memcpy(b, b0, (size_t)len);
+    for (;;) {
+        int db = poly_deg(b, len);
+        if (db < 0) break;
+        int da;
+        while ((da = poly_deg(a, len)) >= db) {      /* a = a mod b */
+            for (int i = 0; i <= db; i++) a[da - db + i] ^= b[i];
+        }
+        uint8_t *t = a; a = b; b = t;                  /* (a, b) = (b, a mod b) */
+    }
+    int d = poly_deg(a, len);
+    free(a); free(b);
+    return d;
+}
+
+/*
+ * Theorem 25.3, condition (3): for every 0 < m < p the polynomials
+ * X^p + 1 and X^m + X + 1 are relatively prime.  Returns 1 if p satisfies it (so that
+ * {Id, g, ..., g^{p-1}, Id+g, ..., Id+g^{p-1}} is a cone, condition (1)), else 0.
+ */
+int oracle_ext_condition(int p) {
+    if (!oracle_valid_p(p)) return 0;
+    int len = p + 1;
+    uint8_t *a = (uint8_t *)calloc((size_t)len, 1), *b = (uint8_t *)calloc((size_t)len, 1);
+    int ok = 1;
+    for (int m = 1; m < p && ok; m++) {
+        memset(a, 0, (size_t)len);
+        memset(b, 0, (size_t)len);
+        a[p] = 1; a[0] = 1;                 /* X^p + 1 */
+        b[m] ^= 1; b[1] ^= 1; b[0] ^= 1;    /* X^m + X + 1 (m = 1 gives 1) */
+        if (poly_gcd_deg(a, b, len) != 0) ok = 0;
+    }
+    free(a); free(b);
+    return ok;
+}
+
+/* Matrix g_k of disk k in Eq. (qext): g^k for 0 <= k < p,
+ * Id + g^{k-p+1} for p <= k <= 2p-2; g = S_p. */
+void oracle_ext_coeff(int p, int k, uint8_t *G) {
+    int n = p - 1;
+    if (k < p) {
+        oracle_sylvester_power(p, k, G);
+    } else {
+        oracle_sylvester_power(p, k - p + 1, G);
+        for (int i = 0; i < n; i++) G[i * n + i] ^= 1;
+    }
+}
+
+static int ext_args_ok(int p, int D) {
+    if (!oracle_valid_p(p) || D < 1 || D > 2 * p - 1) return 0;
+    if (D > p && !oracle_ext_condition(p)) return 0;
+    return 1;
+}
+
+/*
+ * Encode with the extended Q-parity, Eq. (qext), D data disks
+ * (1 <= D <= 2p-1; D > p requires Theorem 25.3):
+ *     P = sum_k d_k,   Q = sum_{k<p} g^k d_k + sum_{k=p}^{D-1} (Id + g^{k-p+1}) d_k,
+ * evaluated per word with the explicit matrices g_k (bit mat-vec).  For D <= p this is the
+ * basic code of Eq. (znparity).
+ */
+int oracle_encode_ext(int p, int D, const uint8_t *const *strips, size_t bytes, uint8_t *P, uint8_t *Q) {
+    if (!ext_args_ok(p, D)) return -1;
+    int n = p - 1;
+    size_t nn = (size_t)n * (size_t)n;
+    size_t W = oracle_word_count(p, bytes);
+    size_t pb = oracle_parity_bytes(p, bytes);
+    uint8_t *G = (uint8_t *)malloc((size_t)D * nn);
+    for (int k = 0; k < D; k++) oracle_ext_coeff(p, k, G + (size_t)k * nn);
+    uint8_t d[ORACLE_MAX_N], t[ORACLE_MAX_N], pw[ORACLE_MAX_N], qw[ORACLE_MAX_N];
+    memset(P, 0, pb);
+    memset(Q, 0, pb);
+    for (size_t w = 0; w < W; w++) {
+        memset(pw, 0, (size_t)n);
+        memset(qw, 0, (size_t)n);
+        for (int k = 0; k < D; k++) {
+            get_word(strips[k], bytes, w, n, d);
+            xor_into(pw, d, n);
+            oracle_gf2_matvec(n, G + (size_t)k * nn, d, t);
+            xor_into(qw, t, n);
+        }
+        put_word(P, pb, w, n, pw);
+        put_word(Q, pb, w, n, qw);
+    }
+    free(G);
+    return 0;
+}
+
+/*
+ * Recovery for the code with coefficients g_k of Eq. (qext), following the constructive
+ * proof of Lemma 23.2 literally, with 0-based indices (data 0..D-1,
+ * P = D, Q = D+1) and inverses by Gauss-Jordan:
+ *   (P, Q):     re-encode;
+ *   (d_j, Q):   d_j = P + sum_{k!=j} d_k, then Q from the second equation;
+ *   (d_j, P):   d_j = g_j^{-1}(Q + sum_{k!=j} g_k d_k), then P = sum_k d_k;
+ *   (d_i, d_j): d_j = (g_i + g_j)^{-1}(g_i P + Q + sum_{k!=i,j} (g_k + g_i) d_k),
+ *               then d_i from the first equation, d_i = P + sum_{k!=i} d_k.
+ * Returns 0, -1 (bad arguments) or -2 (a required matrix is singular).
+ */
+int oracle_recover_ext(int p, int D, int lost_i, int lost_j, uint8_t *const *strips, size_t bytes) {
+    if (!ext_args_ok(p, D)) return -1;
+    if (lost_i == lost_j || lost_i < 0 || lost_j < 0 || lost_i >= D + 2 || lost_j >= D + 2) return -1;
+    int i = lost_i < lost_j ? lost_i : lost_j, j = lost_i < lost_j ? lost_j : lost_i;
+    int n = p - 1;
+    size_t nn = (size_t)n * (size_t)n;
+    size_t W = oracle_word_count(p, bytes);
+    size_t pb = oracle_parity_bytes(p, bytes);
+    const int iP = D, iQ = D + 1;
+    if (i == iP && j == iQ)
+        return oracle_encode_ext(p, D, (const uint8_t *const *)strips, bytes, strips[iP], strips[iQ]);
+    uint8_t *G = (uint8_t *)malloc((size_t)D * nn);
+    for (int k = 0; k < D; k++) oracle_ext_coeff(p, k, G + (size_t)k * nn);
+    uint8_t *A = (uint8_t *)malloc(nn), *M = (uint8_t *)malloc(nn);
+    uint8_t d[ORACLE_MAX_N], t[ORACLE_MAX_N], acc[ORACLE_MAX_N], pw[ORACLE_MAX_N];
+    int rc = 0;
+    if (j == iQ) {                                   /* (d_i, Q) */
+        for (size_t w = 0; w < W; w++) {
+            get_word(strips[iP], pb, w, n, acc);
+            for (int k = 0; k < D; k++) {
+                if (k == i) continue;
+                get_word(strips[k], bytes, w, n, d);
+                xor_into(acc, d, n);
+            }
+            put_word(strips[i], bytes, w, n, acc);
+        }
+        uint8_t *Pd = (uint8_t *)malloc(pb);
+        rc = oracle_encode_ext(p, D, (const uint8_t *const *)strips, bytes, Pd, strips[iQ]);
+        free(Pd);
+    } else if (j == iP) {                            /* (d_i, P) */
+        if (!oracle_gf2_inverse(n, G + (size_t)i * nn, A)) rc = -2;
+        if (rc == 0) {
+            memset(strips[iP], 0, pb);
+            for (size_t w = 0; w < W; w++) {
+                get_word(strips[iQ], pb, w, n, acc);
+                for (int k = 0; k < D; k++) {
+                    if (k == i) continue;
+                    get_word(strips[k], bytes, w, n, d);
+                    oracle_gf2_matvec(n, G + (size_t)k * nn, d, t);
+                    xor_into(acc, t, n);
+                }
+                oracle_gf2_matvec(n, A, acc, t);           /* d_i */
+                put_word(strips[i], bytes, w, n, t);
+                memcpy(pw, t, (size_t)n);
+                for (int k = 0; k < D; k++) {
+                    if (k == i) continue;
+                    get_word(strips[k], bytes, w, n, d);
+                    xor_into(pw, d, n);
+                }
+                put_word(strips[iP], pb, w, n, pw);
+            }
+        }
+    } else {                                         /* (d_i, d_j), both data */
+        for (size_t e = 0; e < nn; e++) M[e] = G[(size_t)i * nn + e] ^ G[(size_t)j * nn + e];
+        if (!oracle_gf2_inverse(n, M, A)) rc = -2;   /* A = (g_i + g_j)^{-1} */
+        uint8_t *Gk = (uint8_t *)malloc(nn);
+        for (size_t w = 0; rc == 0 && w < W; w++) {
+            get_word(strips[iP], pb, w, n, d);
+            oracle_gf2_matvec(n, G + (size_t)i * nn, d, acc);   /* g_i P */
+            get_word(strips[iQ], pb, w, n, d);
+            xor_into(acc, d, n);                                  /* + Q */
+            for (int k = 0; k < D; k++) {
+                if (k == i || k == j) continue;
+                for (size_t e = 0; e < nn; e++) Gk[e] = G[(size_t)k * nn + e] ^ G[(size_t)i * nn + e];
+                get_word(strips[k], bytes, w, n, d);
+                oracle_gf2_matvec(n, Gk, d, t);                   /* + (g_k + g_i) d_k */
+                xor_into(acc, t, n);
+            }
+            oracle_gf2_matvec(n, A, acc, t);                      /* d_j */
+            put_word(strips[j], bytes, w, n, t);
+            get_word(strips[iP], pb, w, n, pw);                   /* d_i = P + sum_{k!=i} d_k */
+            xor_into(pw, t, n);
+            for (int k = 0; k < D; k++) {
+                if (k == i || k == j) continue;
+                get_word(strips[k], bytes, w, n, d);
+                xor_into(pw, d, n);
+            }
+            put_word(strips[i], bytes, w, n, pw);
+        }
+        free(Gk);
+    }
+    free(G); free(A); free(M);
+    return rc;
 }
