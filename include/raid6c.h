@@ -19,7 +19,10 @@
  *   - Data strips are `bytes` long.  P and Q are raid6c_parity_bytes(p, bytes) long: the
  *     data are zero-extended to W = ceil(8*bytes/(p-1)) whole words and the parity holds all
  *     W*(p-1) bits; parity bits past W*(p-1) are written as zero (R5).
- *   - p is an odd prime, 3 <= p <= 257; 1 <= N <= p (R6, R7).
+ *   - p is an odd prime, 3 <= p <= 257 (R7); 1 <= N <= 2p-1 data
+ *     strips.  N <= p is the code of Eq. (znparity).  p < N <= 2p-1 is the extended code of
+ *     Eq. (qext): data strip k >= p has Q-coefficient 1 + x^{k-p+1}; it is
+ *     accepted only when p satisfies Theorem 25.3 (raid6c_ext_supported), else E_INVALID_N.
  *   - Pointers named "device" must be CUDA device memory of the plan's device; the caller
  *     owns all strip memory (the library never allocates or frees it).  A plan owns only
  *     small device/pinned work buffers, freed by raid6c_plan_destroy.
@@ -48,12 +51,12 @@ extern "C" {
 #endif
 
 #define RAID6C_MAX_P 257
-#define RAID6C_MAX_STRIPS (RAID6C_MAX_P + 2)
+#define RAID6C_MAX_STRIPS (2 * RAID6C_MAX_P + 1) /* 2p-1 data strips (extended code) + P + Q */
 
 typedef enum {
     RAID6C_OK = 0,
     RAID6C_E_INVALID_P = 1,     /* p is not an odd prime in [3, 257] */
-    RAID6C_E_INVALID_N = 2,     /* N < 1 or N > p */
+    RAID6C_E_INVALID_N = 2,     /* N < 1, N > 2p-1, or p < N with p failing Theorem 25.3 */
     RAID6C_E_INVALID_INDEX = 3, /* lost index outside [0, N+2) or lost_i == lost_j */
     RAID6C_E_NULL = 4,          /* a required pointer is NULL */
     RAID6C_E_SIZE = 5,          /* bytes == 0, num_stripes < 0, or a stride smaller than its strip */
@@ -85,6 +88,11 @@ int raid6c_valid_p(int p);
 /* 1 if p has a specialised (compile-time-p) TMA kernel, 0 if it runs the generic kernel. */
 int raid6c_has_fast_path(int p);
 
+/* 1 if p satisfies Theorem 25.3: gcd(X^p + 1, X^m + X + 1) = 1 for all
+ * 0 < m < p, so the extended code (up to 2p-1 data strips) recovers every pair.  Fails for the
+ * Mersenne primes and 73 among p <= 257. */
+int raid6c_ext_supported(int p);
+
 /* Static description of the status code (never NULL). */
 const char *raid6c_status_string(raid6c_status s);
 
@@ -108,7 +116,8 @@ raid6c_status raid6c_sync(raid6c_plan plan);
 
 /* ------------------------------------------- north-star single-stripe calls (synchronous) */
 
-/* Encode one stripe on the current CUDA device (Eq. (znparity)).
+/* Encode one stripe on the current CUDA device (Eq. (znparity); Eq. (qext)
+ * when N > p).
  * strips: HOST array of N DEVICE pointers (data strips, `bytes` each);  P, Q: DEVICE
  * pointers of raid6c_parity_bytes(p, bytes).  Synchronous: returns after the kernel has
  * completed, with its status. */

@@ -457,12 +457,24 @@ int oracle_ext_condition(int p) {
 
 /* Matrix g_k of disk k in Eq. (qext): g^k for 0 <= k < p,
  * Id + g^{k-p+1} for p <= k <= 2p-2; g = S_p. */
+/* Column j of S^e is S^e applied to the unit vector e_j: e single Sylvester steps. */
+static void sylvester_power_cols(int p, int e, uint8_t *G) {
+    int n = p - 1;
+    uint8_t v[ORACLE_MAX_N];
+    for (int j = 0; j < n; j++) {
+        memset(v, 0, (size_t)n);
+        v[j] = 1;
+        oracle_mul_xk(p, e, v, v);
+        for (int r = 0; r < n; r++) G[r * n + j] = v[r];
+    }
+}
+
 void oracle_ext_coeff(int p, int k, uint8_t *G) {
     int n = p - 1;
     if (k < p) {
-        oracle_sylvester_power(p, k, G);
+        sylvester_power_cols(p, k, G);
     } else {
-        oracle_sylvester_power(p, k - p + 1, G);
+        sylvester_power_cols(p, k - p + 1, G);
         for (int i = 0; i < n; i++) G[i * n + i] ^= 1;
     }
 }
@@ -573,7 +585,9 @@ int oracle_recover_ext(int p, int D, int lost_i, int lost_j, uint8_t *const *str
     } else {                                         /* (d_i, d_j), both data */
         for (size_t e = 0; e < nn; e++) M[e] = G[(size_t)i * nn + e] ^ G[(size_t)j * nn + e];
         if (!oracle_gf2_inverse(n, M, A)) rc = -2;   /* A = (g_i + g_j)^{-1} */
-        uint8_t *Gk = (uint8_t *)malloc(nn);
+        uint8_t *Gs = (uint8_t *)malloc((size_t)D * nn);          /* g_k + g_i, once per pair */
+        for (int k = 0; k < D; k++)
+            for (size_t e = 0; e < nn; e++) Gs[(size_t)k * nn + e] = G[(size_t)k * nn + e] ^ G[(size_t)i * nn + e];
         for (size_t w = 0; rc == 0 && w < W; w++) {
             get_word(strips[iP], pb, w, n, d);
             oracle_gf2_matvec(n, G + (size_t)i * nn, d, acc);   /* g_i P */
@@ -581,9 +595,8 @@ int oracle_recover_ext(int p, int D, int lost_i, int lost_j, uint8_t *const *str
             xor_into(acc, d, n);                                  /* + Q */
             for (int k = 0; k < D; k++) {
                 if (k == i || k == j) continue;
-                for (size_t e = 0; e < nn; e++) Gk[e] = G[(size_t)k * nn + e] ^ G[(size_t)i * nn + e];
                 get_word(strips[k], bytes, w, n, d);
-                oracle_gf2_matvec(n, Gk, d, t);                   /* + (g_k + g_i) d_k */
+                oracle_gf2_matvec(n, Gs + (size_t)k * nn, d, t);  /* + (g_k + g_i) d_k */
                 xor_into(acc, t, n);
             }
             oracle_gf2_matvec(n, A, acc, t);                      /* d_j */
@@ -597,7 +610,7 @@ int oracle_recover_ext(int p, int D, int lost_i, int lost_j, uint8_t *const *str
             }
             put_word(strips[i], bytes, w, n, pw);
         }
-        free(Gk);
+        free(Gs);
     }
     free(G); free(A); free(M);
     return rc;

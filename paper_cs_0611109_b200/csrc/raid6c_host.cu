@@ -73,6 +73,115 @@ bool is_valid_p(int p) {
 size_t word_count(int p, size_t bytes) { return (8 * bytes + (p - 2)) / (p - 1); }
 size_t parity_bytes(int p, size_t bytes) { return (word_count(p, bytes) * (p - 1) + 7) / 8; }
 
+// ------------------------------------------------ F2[X] polynomials (64-bit limbs), host only
+struct Poly {
+  static constexpr int L = 10;  // 640 bits: products of two degree-<=257 polynomials fit
+  uint64_t w[L] = {};
+  int deg() const {
+    for (int i = L - 1; i >= 0; i--)
+      if (w[i]) return 64 * i + 63 - __builtin_clzll(w[i]);
+    return -1;
+  }
+  bool bit(int i) const { return (w[i >> 6] >> (i & 63)) & 1u; }
+  void flip(int i) { w[i >> 6] ^= 1ull << (i & 63); }
+  void xor_shifted(const Poly& b, int sh) {  // this ^= b * X^sh
+    const int q = sh >> 6, r = sh & 63;
+    for (int i = L - 1; i >= q; i--) {
+      uint64_t v = b.w[i - q] << r;
+      if (r && i - q - 1 >= 0) v |= b.w[i - q - 1] >> (64 - r);
+      w[i] ^= v;
+    }
+  }
+  bool is_one() const {
+    if (w[0] != 1) return false;
+    for (int i = 1; i < L; i++)
+      if (w[i]) return false;
+    return true;
+  }
+  bool is_zero() const { return deg() < 0; }
+};
+
+Poly pmul(const Poly& a, const Poly& b) {
+  Poly r;
+  for (int i = 0, d = a.deg(); i <= d; i++)
+    if (a.bit(i)) r.xor_shifted(b, i);
+  return r;
+}
+void pdivmod(Poly a, const Poly& b, Poly& q, Poly& r) {  // a = q b + r
+  q = Poly();
+  const int db = b.deg();
+  for (int da = a.deg(); da >= db; da = a.deg()) {
+    q.flip(da - db);
+    a.xor_shifted(b, da - db);
+  }
+  r = a;
+}
+Poly pgcd(Poly a, Poly b) {
+  while (!b.is_zero()) {
+    Poly q, r;
+    pdivmod(a, b, q, r);
+    a = b;
+    b = r;
+  }
+  return a;
+}
+
+// Theorem 25.3 condition (3): gcd(X^p + 1, X^m + X + 1) = 1 for 0 < m < p.
+bool ext_supported_p(int p) {
+  Poly xp1;
+  xp1.flip(p);
+  xp1.flip(0);
+  for (int m = 1; m < p; m++) {
+    Poly t;
+    t.flip(m);
+    t.flip(1);
+    t.flip(0);
+    if (!pgcd(xp1, t).is_one()) return false;
+  }
+  return true;
+}
+
+// Ring R_p = F2[X]/(Phi_p), Phi_p = 1 + X + ... + X^{p-1}.
+Poly phi(int p) {
+  Poly f;
+  for (int i = 0; i < p; i++) f.flip(i);
+  return f;
+}
+Poly ring_reduce(const Poly& a, int p) {
+  Poly q, r;
+  pdivmod(a, phi(p), q, r);
+  return r;
+}
+// Q-coefficient of data strip k in Eq. (qext): X^k (k < p) or 1 + X^{k-p+1}, reduced.
+Poly ext_coeff(int p, int k) {
+  Poly c;
+  if (k < p) {
+    c.flip(k);
+  } else {
+    c.flip(0);
+    c.flip(k - p + 1);
+  }
+  return ring_reduce(c, p);
+}
+// Inverse in R_p by the extended Euclidean algorithm; false if a is not a unit.
+bool ring_inverse(const Poly& a, int p, Poly& inv) {
+  Poly r0 = phi(p), r1 = ring_reduce(a, p), s0, s1;
+  s1.flip(0);
+  while (!r1.is_zero()) {
+    Poly q, r;
+    pdivmod(r0, r1, q, r);
+    r0 = r1;
+    r1 = r;
+    Poly t = pmul(q, s1);
+    for (int i = 0; i < Poly::L; i++) t.w[i] ^= s0.w[i];
+    s0 = s1;
+    s1 = t;
+  }
+  if (!r0.is_one()) return false;
+  inv = ring_reduce(s0, p);
+  return true;
+}
+
 // per-(device, kernel) one-time attribute setup
 std::mutex g_attr_mu;
 std::map<std::pair<int, const void*>, int> g_occ;  // -> CTAs per SM
@@ -104,6 +213,11 @@ struct raid6c_plan_s {
   const zp::FastEntry* fe = nullptr;
   int num_sms = 148;
   int occ[4] = {1, 1, 1, 1};  // CTAs per SM per kernel mode
+  int occ_ext[4] = {1, 1, 1, 1};
+  bool ext = false;           // N > p: extended code of Eq. (qext)
+  std::mutex mu;              // serialises the shared single-stripe plans' program buffer
+  zp::ExtProg* d_prog = nullptr;
+  size_t prog_cap = 0;
   int2* d_er = nullptr;
   size_t er_cap = 0;
   raid6c_status sticky = RAID6C_OK;
@@ -133,7 +247,7 @@ struct DeviceGuard {
 
 raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, cudaStream_t stream) {
   if (!is_valid_p(p)) return RAID6C_E_INVALID_P;
-  if (N < 1 || N > p) return RAID6C_E_INVALID_N;
+  if (N < 1 || N > 2 * p - 1 || (N > p && !ext_supported_p(p))) return RAID6C_E_INVALID_N;
   if (bytes == 0) return RAID6C_E_SIZE;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0 || device < 0 || device >= ndev) {
@@ -154,12 +268,15 @@ raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, 
   pl->device = device;
   pl->stream = stream;
   pl->num_sms = prop.multiProcessorCount;
+  pl->ext = N > p;
   pl->fe = zp::fast_entry(p);
+  if (pl->fe && pl->ext && !pl->fe->kernel_ext[0]) pl->fe = nullptr;  // no fast extended kernels: generic
   if (pl->fe) {
     DeviceGuard g(device);
     for (int m = 0; m < 4; m++) {
-      raid6c_status st = kernel_occupancy(device, pl->fe->kernel[m], pl->fe->threads + 32, pl->fe->smem_bytes[m],
-                                          &pl->occ[m]);
+      const void* k = pl->ext ? pl->fe->kernel_ext[m] : pl->fe->kernel[m];
+      const size_t sm = pl->ext ? pl->fe->smem_ext[m] : pl->fe->smem_bytes[m];
+      raid6c_status st = kernel_occupancy(device, k, pl->fe->threads + 32, sm, &pl->occ[m]);
       if (st != RAID6C_OK) return st;
     }
   }
@@ -169,6 +286,7 @@ raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, 
 void plan_release(raid6c_plan pl) {
   DeviceGuard g(pl->device);
   if (pl->d_er) cudaFree(pl->d_er);
+  if (pl->d_prog) cudaFree(pl->d_prog);
   if (pl->d_stage) cudaFree(pl->d_stage);
   for (int i = 0; i < 3; i++)
     if (pl->hs[i]) cudaStreamDestroy(pl->hs[i]);
@@ -207,8 +325,8 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
     uint64_t grid = std::min<uint64_t>(cap, std::max<uint64_t>(items, tail_ctas));
     if (grid == 0) grid = 1;
     void* args[] = {&a};
-    err = cudaLaunchKernel(fe->kernel[mode], dim3(static_cast<unsigned>(grid)), dim3(fe->threads + 32), args,
-                           fe->smem_bytes[mode], st);
+    err = cudaLaunchKernel(pl->ext ? fe->kernel_ext[mode] : fe->kernel[mode], dim3(static_cast<unsigned>(grid)),
+                           dim3(fe->threads + 32), args, pl->ext ? fe->smem_ext[mode] : fe->smem_bytes[mode], st);
   } else {
     err = zp::generic_launch(a, pl->p, mode, st, pl->num_sms);
   }
@@ -267,6 +385,57 @@ raid6c_status upload_erasures(raid6c_plan pl, const raid6c_erasure* er, int coun
   }
   // pageable source: the copy is staged before this call returns, so `h` may be freed
   ZP_CUDA(cudaMemcpyAsync(pl->d_er, h.data(), count * sizeof(int2), cudaMemcpyHostToDevice, st));
+  return RAID6C_OK;
+}
+
+// Extended code: per-stripe multiplier u for the DP / DD solves (ExtProg), uploaded into the
+// plan's device buffer.  pairs: canonical (x < y) per stripe.
+raid6c_status upload_programs(raid6c_plan pl, const std::vector<int2>& pairs, cudaStream_t st) {
+  const int p = pl->p, N = pl->N, S = static_cast<int>(pairs.size());
+  std::vector<zp::ExtProg> h(S);
+  std::map<std::pair<int, int>, int> memo;
+  for (int s = 0; s < S; s++) {
+    const int x = pairs[s].x, y = pairs[s].y;
+    auto it = memo.find({x, y});
+    if (it != memo.end()) {
+      h[s] = h[it->second];
+      continue;
+    }
+    zp::ExtProg& pr = h[s];
+    pr.nu = 0;
+    Poly c;
+    bool need = true;
+    if (y == N + 1 || (x == N && y == N + 1)) need = false;  // DQ / PQ: no solve
+    else if (y == N) c = ext_coeff(p, x);                     // DP: u = g_x^{-1}
+    else {                                                    // DD: u = (g_x + g_y)^{-1}
+      c = ext_coeff(p, x);
+      Poly cy = ext_coeff(p, y);
+      for (int i = 0; i < Poly::L; i++) c.w[i] ^= cy.w[i];
+    }
+    if (need) {
+      Poly u;
+      if (!ring_inverse(c, p, u)) {
+        g_last_err = "extended code: coefficient not invertible";
+        return RAID6C_E_INVALID_N;
+      }
+      for (int i = 0; i < p - 1; i++)
+        if (u.bit(i)) pr.e[pr.nu++] = static_cast<uint16_t>(i);
+    }
+    memo[{x, y}] = s;
+  }
+  if (static_cast<size_t>(S) > pl->prog_cap) {
+    DeviceGuard g(pl->device);
+    if (pl->d_prog) {
+      ZP_CUDA(cudaStreamSynchronize(st));
+      cudaFree(pl->d_prog);
+      pl->d_prog = nullptr;
+    }
+    const size_t cap = std::max<size_t>(64, static_cast<size_t>(S));
+    ZP_CUDA(cudaMalloc(&pl->d_prog, cap * sizeof(zp::ExtProg)));
+    pl->prog_cap = cap;
+  }
+  // pageable source: the copy is staged before this call returns, so `h` may be freed
+  ZP_CUDA(cudaMemcpyAsync(pl->d_prog, h.data(), S * sizeof(zp::ExtProg), cudaMemcpyHostToDevice, st));
   return RAID6C_OK;
 }
 
@@ -383,6 +552,10 @@ raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_
     for (int s = 0; s < num_stripes; s++) ev[s] = {pairs[s].x, pairs[s].y};
     st = upload_erasures(pl, ev.data(), num_stripes, s_k);
     if (st != RAID6C_OK) return st;
+    if (pl->ext) {
+      st = upload_programs(pl, pairs, s_k);
+      if (st != RAID6C_OK) return st;
+    }
   }
   // order after anything already queued on the plan stream
   ZP_CUDA(cudaEventRecord(pl->ev_out[0], pl->stream));
@@ -444,6 +617,10 @@ raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_
     if (recover) {
       a.er = pl->d_er + s0;
       a.er_stride = 1;
+      if (pl->ext) {
+        a.prog = pl->d_prog + s0;
+        a.prog_stride = 1;
+      }
     }
     st = launch(pl, a, recover ? zp::KMODE_RECOVER : zp::KMODE_ENCODE, s_k);
     if (st != RAID6C_OK) return st;
@@ -497,6 +674,7 @@ size_t raid6c_word_count(int p, size_t bytes) { return is_valid_p(p) ? word_coun
 size_t raid6c_parity_bytes(int p, size_t bytes) { return is_valid_p(p) ? parity_bytes(p, bytes) : 0; }
 int raid6c_valid_p(int p) { return is_valid_p(p) ? 1 : 0; }
 int raid6c_has_fast_path(int p) { return zp::fast_entry(p) != nullptr ? 1 : 0; }
+int raid6c_ext_supported(int p) { return is_valid_p(p) && ext_supported_p(p) ? 1 : 0; }
 uint64_t raid6c_launch_count(void) { return g_launches.load(); }
 const char* raid6c_last_cuda_error(void) { return g_last_err.c_str(); }
 
@@ -504,7 +682,7 @@ const char* raid6c_status_string(raid6c_status s) {
   switch (s) {
     case RAID6C_OK: return "ok";
     case RAID6C_E_INVALID_P: return "p is not an odd prime in [3, 257]";
-    case RAID6C_E_INVALID_N: return "N must satisfy 1 <= N <= p";
+    case RAID6C_E_INVALID_N: return "N must satisfy 1 <= N <= p, or p < N <= 2p-1 with p satisfying Theorem 25.3";
     case RAID6C_E_INVALID_INDEX: return "lost strip index out of range or repeated";
     case RAID6C_E_NULL: return "null pointer argument";
     case RAID6C_E_SIZE: return "invalid size or stride";
@@ -561,7 +739,7 @@ raid6c_status raid6c_sync(raid6c_plan plan) {
 
 raid6c_status raid6c_encode(int p, int N, const uint8_t* const* strips, uint8_t* P, uint8_t* Q, size_t bytes) {
   if (!is_valid_p(p)) return RAID6C_E_INVALID_P;
-  if (N < 1 || N > p) return RAID6C_E_INVALID_N;
+  if (N < 1 || N > 2 * p - 1 || (N > p && !ext_supported_p(p))) return RAID6C_E_INVALID_N;
   if (bytes == 0) return RAID6C_E_SIZE;
   if (!strips || !P || !Q) return RAID6C_E_NULL;
   for (int k = 0; k < N; k++)
@@ -586,7 +764,7 @@ raid6c_status raid6c_encode(int p, int N, const uint8_t* const* strips, uint8_t*
 
 raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* const* strips, size_t bytes) {
   if (!is_valid_p(p)) return RAID6C_E_INVALID_P;
-  if (N < 1 || N > p) return RAID6C_E_INVALID_N;
+  if (N < 1 || N > 2 * p - 1 || (N > p && !ext_supported_p(p))) return RAID6C_E_INVALID_N;
   if (bytes == 0) return RAID6C_E_SIZE;
   raid6c_status st = check_erasure(N, lost_i, lost_j);
   if (st != RAID6C_OK) return st;
@@ -602,6 +780,13 @@ raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* cons
   a.num_stripes = 1;
   a.ei = std::min(lost_i, lost_j);
   a.ej = std::max(lost_i, lost_j);
+  std::unique_lock<std::mutex> lk(pl->mu);
+  if (pl->ext) {
+    st = upload_programs(pl, {make_int2(a.ei, a.ej)}, nullptr);
+    if (st != RAID6C_OK) return st;
+    a.prog = pl->d_prog;
+    a.prog_stride = 0;
+  }
   st = launch(pl, a, zp::KMODE_RECOVER, nullptr);
   if (st != RAID6C_OK) return st;
   ZP_CUDA(cudaStreamSynchronize(nullptr));
@@ -627,6 +812,24 @@ raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t* data, size_t str
   if (!erasures) return RAID6C_E_NULL;
   if (num_erasures != 1 && num_erasures != num_stripes) return RAID6C_E_SIZE;
   DeviceGuard g(plan->device);
+  if (plan->ext) {  // extended code: per-stripe multipliers are built on the host from the pairs
+    std::vector<raid6c_erasure> hp(num_erasures);
+    if (erasures_on_device) {
+      ZP_CUDA(cudaMemcpy(hp.data(), erasures, num_erasures * sizeof(raid6c_erasure), cudaMemcpyDeviceToHost));
+    } else {
+      std::copy(erasures, erasures + num_erasures, hp.begin());
+    }
+    std::vector<int2> pairs(num_erasures);
+    for (int s2 = 0; s2 < num_erasures; s2++) {
+      st = check_erasure(plan->N, hp[s2].lost_i, hp[s2].lost_j);
+      if (st != RAID6C_OK) return st;
+      pairs[s2] = make_int2(std::min(hp[s2].lost_i, hp[s2].lost_j), std::max(hp[s2].lost_i, hp[s2].lost_j));
+    }
+    st = upload_programs(plan, pairs, plan->stream);
+    if (st != RAID6C_OK) return st;
+    a.prog = plan->d_prog;
+    a.prog_stride = num_erasures == 1 ? 0 : 1;
+  }
   if (erasures_on_device) {
     a.er = reinterpret_cast<const int2*>(erasures);
     a.er_stride = num_erasures == 1 ? 0 : 1;

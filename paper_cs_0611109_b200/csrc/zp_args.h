@@ -8,6 +8,14 @@
 
 namespace zp {
 
+// Extended code (NEXT-2, N > p): per-stripe multiplier u for the DP / DD solves, a ring element
+// of R_p given by the exponents of its nonzero coefficients (u = sum_i x^{e_i}), computed on the
+// host: u = g_j^{-1} (DP) or (g_x + g_y)^{-1} (DD), g_k the Eq. (qext) coefficient of disk k.
+struct ExtProg {
+  int32_t nu;
+  uint16_t e[RAID6C_MAX_P - 1];
+};
+
 // One launch = a batch of stripes with a common (p, N, bytes).  Strip k of stripe s lives
 // at base[k] + s * (k < N ? data_stride : parity_stride).
 struct ZpArgs {
@@ -36,6 +44,9 @@ struct ZpArgs {
   const uint8_t* nbase;
   uint64_t new_stride;
   uint32_t* counts;
+  // NEXT-2: multiplier programs for the extended code (prog[s * prog_stride]); N > p only.
+  const ExtProg* prog;
+  int prog_stride;
 };
 
 // Kernel-geometry record for one compiled prime (fast path) -- filled by each
@@ -47,6 +58,8 @@ struct FastEntry {
   int threads;      // consumer threads (+32 producer threads per CTA)
   const void* kernel[4];  // __global__ void(ZpArgs) per mode: encode, recover, scrub, update
   size_t smem_bytes[4];
+  const void* kernel_ext[4];  // extended-code (N > p) kernels, nullptr if p fails Theorem 25.3
+  size_t smem_ext[4];
 };
 
 const FastEntry* fast_entry(int p);  // nullptr if p has no fast path

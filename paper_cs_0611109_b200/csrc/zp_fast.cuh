@@ -287,7 +287,7 @@ struct ItemDesc {
   int base;   // rotation origin: amounts are (k - base) mod p
 };
 
-template <int MODE>
+template <int MODE, bool EXT = false>
 __device__ __forceinline__ ItemDesc item_desc(const ZpArgs& a, int s) {
   ItemDesc d;
   if constexpr (MODE == MODE_SCRUB) {
@@ -315,7 +315,9 @@ __device__ __forceinline__ ItemDesc item_desc(const ZpArgs& a, int s) {
     d.y = i < j ? j : i;
     if (d.y == a.N + 1) d.cls = (d.x == a.N) ? CLS_PQ : CLS_DQ;
     else d.cls = (d.y == a.N) ? CLS_DP : CLS_DD;
-    d.base = (d.cls == CLS_DP || d.cls == CLS_DD) ? d.x : 0;
+    // basic code: move the rotation origin to the lost strip (x^{-x} folded into the amounts);
+    // extended code: origin 0, the solve multiplies by a host-computed u (ExtProg)
+    d.base = (!EXT && (d.cls == CLS_DP || d.cls == CLS_DD)) ? d.x : 0;
     return d;
   }
 }
@@ -354,8 +356,21 @@ __device__ __forceinline__ const uint8_t* row_ptr(const ZpArgs& a, int k, int s)
 }
 __device__ __forceinline__ uint64_t row_len(const ZpArgs& a, int k) { return k < a.N ? a.bytes : a.pbytes; }
 
-// Fold one source row into the accumulators (P part and rotated Q part).
+// acc += g_k * S for the extended code's coefficient of data strip k (Eq. (qext)):
+// x^k for k < p, 1 + x^{k-p+1} for k >= p.
 template <class G>
+__device__ __forceinline__ void add_ext_coeff(const uint32_t (&S)[G::C], int k, const uint2* __restrict__ mtab,
+                                              Acc<G>& acc) {
+  if (k < G::P) {
+    rot_acc<G>(S, k, mtab, acc);
+  } else {
+    rot_acc<G>(S, 0, mtab, acc);
+    rot_acc<G>(S, k - G::P + 1, mtab, acc);
+  }
+}
+
+// Fold one source row into the accumulators (P part and rotated Q part).
+template <class G, bool EXT = false>
 __device__ __forceinline__ void fold_row(const ZpArgs& a, const ItemDesc& d, int k, const uint32_t (&L)[G::C],
                                          const uint2* __restrict__ mtab, uint32_t (&Pa)[G::C], Acc<G>& acc) {
   if (k <= a.N) {  // data strips and P feed the P accumulator
@@ -363,10 +378,66 @@ __device__ __forceinline__ void fold_row(const ZpArgs& a, const ItemDesc& d, int
     for (int l = 0; l < G::C; l++) Pa[l] ^= L[l];
   }
   if (k != a.N) {  // data strips and Q feed the rotated accumulator
-    int amt = (k < a.N) ? (k - d.base) : (G::P - d.base);
-    amt %= G::P;
-    if (amt < 0) amt += G::P;
-    rot_acc<G>(L, amt, mtab, acc);
+    if constexpr (EXT) {
+      if (k < a.N) add_ext_coeff<G>(L, k, mtab, acc);
+      else rot_acc<G>(L, 0, mtab, acc);  // Q
+    } else {
+      int amt = (k < a.N) ? (k - d.base) : (G::P - d.base);
+      amt %= G::P;
+      if (amt < 0) amt += G::P;
+      rot_acc<G>(L, amt, mtab, acc);
+    }
+  }
+}
+
+// out = u * t for a host-computed ring element u = sum_i x^{e_i} (ExtProg), t reduced.
+template <class G>
+__device__ __forceinline__ void mul_prog(const uint32_t (&t)[G::C], const ExtProg* __restrict__ pr,
+                                         const uint2* __restrict__ mtab, uint32_t (&out)[G::C]) {
+  Acc<G> acc;
+  acc.zero();
+  const int nu = pr->nu;
+#pragma unroll 1
+  for (int i = 0; i < nu; i++) rot_acc<G>(t, pr->e[i], mtab, acc);
+  reduce<G>(acc, out);
+}
+
+// Extended-code class epilogue (Lemma 23.2 proof, with g_k of Eq. (qext)):
+//   PQ: re-encode;  DQ: d_j = P + sum d_k, Q += g_j d_j;
+//   DP: d_j = u (Q + sum_{k!=j} g_k d_k), u = g_j^{-1};  P = sum d_k
+//   DD: d_y = u (g_x dP + dQ), u = (g_x + g_y)^{-1};  d_x = d_y + dP
+template <class G>
+__device__ __forceinline__ void finish_ext(const ZpArgs& a, const ItemDesc& d, int s, uint32_t (&Pa)[G::C], Acc<G>& acc,
+                                           const uint2* __restrict__ mtab, uint32_t (&o0)[G::C],
+                                           uint32_t (&o1)[G::C], int& k0, int& k1) {
+  constexpr int C = G::C;
+  const ExtProg* pr = a.prog + static_cast<int64_t>(s) * a.prog_stride;
+  if (d.cls == CLS_PQ) {
+#pragma unroll
+    for (int l = 0; l < C; l++) o0[l] = Pa[l];
+    reduce<G>(acc, o1);
+    k0 = a.N; k1 = a.N + 1;
+  } else if (d.cls == CLS_DQ) {
+#pragma unroll
+    for (int l = 0; l < C; l++) o0[l] = Pa[l];
+    add_ext_coeff<G>(o0, d.x, mtab, acc);
+    reduce<G>(acc, o1);
+    k0 = d.x; k1 = a.N + 1;
+  } else if (d.cls == CLS_DP) {
+    uint32_t t[C];
+    reduce<G>(acc, t);
+    mul_prog<G>(t, pr, mtab, o0);
+#pragma unroll
+    for (int l = 0; l < C; l++) o1[l] = Pa[l] ^ o0[l];
+    k0 = d.x; k1 = a.N;
+  } else {
+    add_ext_coeff<G>(Pa, d.x, mtab, acc);
+    uint32_t t[C];
+    reduce<G>(acc, t);
+    mul_prog<G>(t, pr, mtab, o1);
+#pragma unroll
+    for (int l = 0; l < C; l++) o0[l] = o1[l] ^ Pa[l];
+    k0 = d.x; k1 = d.y;
   }
 }
 
@@ -466,7 +537,7 @@ struct Layout {
 
 // Per-item epilogue for every mode: fills the NOUT output chunks and their strip indices
 // (scrub: adds the count of words violating a parity equation to a.counts[s]).
-template <int MODE, class G, bool WARP_UNIFORM = true>
+template <int MODE, class G, bool WARP_UNIFORM = true, bool EXT = false>
 __device__ __forceinline__ void epilogue(const ZpArgs& a, const ItemDesc& d, int s, uint32_t (&Pa)[G::C], Acc<G>& acc,
                                          const uint32_t (&NEW)[G::C], const uint2* __restrict__ mtab,
                                          uint32_t (&o0)[G::C], uint32_t (&o1)[G::C], int& k0, int& k1, int& k2) {
@@ -489,12 +560,14 @@ __device__ __forceinline__ void epilogue(const ZpArgs& a, const ItemDesc& d, int
     for (int l = 0; l < C; l++) o0[l] = Pa[l];
     reduce<G>(acc, o1);
     k0 = a.N; k1 = a.N + 1; k2 = d.x;
+  } else if constexpr (EXT) {
+    finish_ext<G>(a, d, s, Pa, acc, mtab, o0, o1, k0, k1);
   } else {
     finish<G>(a, d, Pa, acc, mtab, o0, o1, k0, k1);
   }
 }
 
-template <int P, int MODE>
+template <int P, int MODE, bool EXT = false>
 __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __grid_constant__ ZpArgs a) {
   using G = Geo<P>;
   using LY = Layout<P, MODE>;
@@ -541,7 +614,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
       for (uint64_t it = blockIdx.x; it < body_items; it += gridDim.x) {
         const int s = static_cast<int>(it / tiles);
         const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
-        const ItemDesc d = item_desc<MODE>(a, s);
+        const ItemDesc d = item_desc<MODE, EXT>(a, s);
         for (int r = 0; r < R; r++) {
           const uint8_t* g = row_ptr(a, row_strip<MODE>(a, r, d), s) + t * TB;
           mbar_wait(&empty[stage], ph ^ 1u);
@@ -559,7 +632,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
   for (uint64_t it = blockIdx.x; it < body_items; it += gridDim.x) {
     const int s = static_cast<int>(it / tiles);
     const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
-    const ItemDesc d = item_desc<MODE>(a, s);
+    const ItemDesc d = item_desc<MODE, EXT>(a, s);
     uint32_t Pa[C];
     uint32_t NEW[C];  // unused in the body path (update stages the new row in SMEM)
     Acc<G> acc;
@@ -581,7 +654,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
           st_chunk_smem<C>(outb + 2 * TB + tid * CB, L);
         }
       }
-      fold_row<G>(a, d, k, L, mtab, Pa, acc);
+      fold_row<G, EXT>(a, d, k, L, mtab, Pa, acc);
       // Release the stage only after every loaded lane has been consumed: an mbarrier.arrive
       // issued right after the LDS does not wait for the loads to complete, and the producer's
       // next TMA write (async proxy) can then overwrite the row under a lagging warp's reads.
@@ -591,7 +664,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
     }
     uint32_t o0[C], o1[C];
     int k0 = 0, k1 = 0, k2 = 0;
-    epilogue<MODE, G>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+    epilogue<MODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
     if constexpr (NOUT > 0) {
       if constexpr (MODE != MODE_UPDATE) {  // (update waited at the start of the item)
         if (tid == 0) bulk_wait_read0();  // previous item's bulk stores have read outb
@@ -618,7 +691,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
        u += static_cast<uint64_t>(gridDim.x) * NT) {
     const int s = static_cast<int>(u / tups);
     const uint64_t off = body_end + (u - static_cast<uint64_t>(s) * tups) * CB;
-    const ItemDesc d = item_desc<MODE>(a, s);
+    const ItemDesc d = item_desc<MODE, EXT>(a, s);
     uint32_t Pa[C];
     uint32_t NEW[C];  // update mode only (dead otherwise)
     Acc<G> acc;
@@ -636,14 +709,14 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
           st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k, s)) + off, off, row_len(a, k), L);
         }
       }
-      fold_row<G>(a, d, k, L, mtab, Pa, acc);
+      fold_row<G, EXT>(a, d, k, L, mtab, Pa, acc);
     }
     uint32_t o0[C], o1[C];
     int k0 = 0, k1 = 0, k2 = 0;
     if constexpr (MODE == MODE_SCRUB) {  // lanes of a warp may work on different stripes here
-      epilogue<MODE, G, false>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+      epilogue<MODE, G, false, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
     } else {
-      epilogue<MODE, G>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+      epilogue<MODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
       st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k0, s)) + off, off, row_len(a, k0), o0);
       st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k1, s)) + off, off, row_len(a, k1), o1);
     }
@@ -652,10 +725,10 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
     if (tid == 0) bulk_wait0();
 }
 
-template <int P>
+template <int P, bool WITH_EXT>
 FastEntry make_entry() {
   using G = Geo<P>;
-  FastEntry e;
+  FastEntry e{};
   e.p = P;
   e.chunk_bytes = G::CB;
   e.tile_bytes = G::TB;
@@ -668,19 +741,40 @@ FastEntry make_entry() {
   e.smem_bytes[MODE_RECOVER] = Layout<P, MODE_RECOVER>::SMEM;
   e.smem_bytes[MODE_SCRUB] = Layout<P, MODE_SCRUB>::SMEM;
   e.smem_bytes[MODE_UPDATE] = Layout<P, MODE_UPDATE>::SMEM;
+  if constexpr (WITH_EXT) {
+    e.kernel_ext[MODE_ENCODE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_ENCODE, true>);
+    e.kernel_ext[MODE_RECOVER] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_RECOVER, true>);
+    e.kernel_ext[MODE_SCRUB] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_SCRUB, true>);
+    e.kernel_ext[MODE_UPDATE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_UPDATE, true>);
+    e.smem_ext[MODE_ENCODE] = Layout<P, MODE_ENCODE>::SMEM;
+    e.smem_ext[MODE_RECOVER] = Layout<P, MODE_RECOVER>::SMEM;
+    e.smem_ext[MODE_SCRUB] = Layout<P, MODE_SCRUB>::SMEM;
+    e.smem_ext[MODE_UPDATE] = Layout<P, MODE_UPDATE>::SMEM;
+  }
   return e;
 }
 
 }  // namespace zp
 
-#define ZP_INSTANTIATE_FAST(PP)                                                        \
-  namespace zp {                                                                       \
-  template __global__ void zp_kernel<PP, MODE_ENCODE>(const __grid_constant__ ZpArgs);  \
-  template __global__ void zp_kernel<PP, MODE_RECOVER>(const __grid_constant__ ZpArgs); \
-  template __global__ void zp_kernel<PP, MODE_SCRUB>(const __grid_constant__ ZpArgs);   \
-  template __global__ void zp_kernel<PP, MODE_UPDATE>(const __grid_constant__ ZpArgs);  \
-  const FastEntry* fast_entry_##PP() {                                                 \
-    static const FastEntry e = make_entry<PP>();                                       \
-    return &e;                                                                         \
-  }                                                                                    \
+// Basic-code kernels for p (all four modes); WITH_EXT also instantiates the extended-code
+// (Eq. (qext), N > p) kernels -- only for primes satisfying Theorem 25.3.
+#define ZP_INSTANTIATE_FAST_IMPL(PP, WITH_EXT)                                               \
+  namespace zp {                                                                             \
+  template __global__ void zp_kernel<PP, MODE_ENCODE>(const __grid_constant__ ZpArgs);        \
+  template __global__ void zp_kernel<PP, MODE_RECOVER>(const __grid_constant__ ZpArgs);       \
+  template __global__ void zp_kernel<PP, MODE_SCRUB>(const __grid_constant__ ZpArgs);         \
+  template __global__ void zp_kernel<PP, MODE_UPDATE>(const __grid_constant__ ZpArgs);        \
+  const FastEntry* fast_entry_##PP() {                                                       \
+    static const FastEntry e = make_entry<PP, WITH_EXT>();                                   \
+    return &e;                                                                               \
+  }                                                                                          \
   }
+#define ZP_INSTANTIATE_FAST(PP) ZP_INSTANTIATE_FAST_IMPL(PP, false)
+#define ZP_INSTANTIATE_FAST_EXT(PP)                                                          \
+  namespace zp {                                                                             \
+  template __global__ void zp_kernel<PP, MODE_ENCODE, true>(const __grid_constant__ ZpArgs);  \
+  template __global__ void zp_kernel<PP, MODE_RECOVER, true>(const __grid_constant__ ZpArgs); \
+  template __global__ void zp_kernel<PP, MODE_SCRUB, true>(const __grid_constant__ ZpArgs);   \
+  template __global__ void zp_kernel<PP, MODE_UPDATE, true>(const __grid_constant__ ZpArgs);  \
+  }                                                                                          \
+  ZP_INSTANTIATE_FAST_IMPL(PP, true)

@@ -1,3 +1,3 @@
 // zp_fast_p257.cu -- fast-path instantiation for p = 257 (see zp_fast.cuh).
 #include "zp_fast.cuh"
-ZP_INSTANTIATE_FAST(257)
+ZP_INSTANTIATE_FAST_EXT(257)

@@ -71,7 +71,7 @@ struct Desc {
   int x, y, cls, base;  // cls: 0 PQ, 1 DQ, 2 DP, 3 DD, 4 scrub, 5 update (x = rewritten strip)
 };
 
-__device__ Desc desc_of(const ZpArgs& a, int s, int mode) {
+__device__ Desc desc_of(const ZpArgs& a, int s, int mode, int p) {
   Desc d;
   if (mode == KMODE_SCRUB) {
     d.x = d.y = -1; d.cls = 4; d.base = 0;
@@ -95,8 +95,26 @@ __device__ Desc desc_of(const ZpArgs& a, int s, int mode) {
   d.y = i < j ? j : i;
   if (d.y == a.N + 1) d.cls = (d.x == a.N) ? 0 : 1;  // PQ : DQ
   else d.cls = (d.y == a.N) ? 2 : 3;                  // DP : DD
-  d.base = (d.cls == 2 || d.cls == 3) ? d.x : 0;
+  // basic code: rotation origin at the lost strip; extended code (N > p): origin 0 + ExtProg
+  d.base = (a.N <= p && (d.cls == 2 || d.cls == 3)) ? d.x : 0;
   return d;
+}
+
+// acc ^= g_k * v with g_k the Eq. (qext) coefficient of data strip k (x^k, or 1 + x^{k-p+1}).
+__device__ void add_coeff(Word& acc, const Word& v, int k, int p) {
+  if (k < p) {
+    rot_acc(acc, v, k, p);
+  } else {
+    rot_acc(acc, v, 0, p);
+    rot_acc(acc, v, k - p + 1, p);
+  }
+}
+
+// out = u * t, u = sum_i x^{e_i} from the stripe's ExtProg.
+__device__ void mul_prog(const Word& t, const ExtProg* pr, int p, Word& out) {
+  wzero(out);
+  for (int i = 0; i < pr->nu; i++) rot_acc(out, t, pr->e[i], p);
+  reduce(out, p);
 }
 
 __device__ __forceinline__ uint64_t sstride(const ZpArgs& a, int k) { return k < a.N ? a.data_stride : a.parity_stride; }
@@ -120,7 +138,8 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
        u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int s = static_cast<int>(u / groups);
     const uint64_t grp = u - static_cast<uint64_t>(s) * groups;
-    const Desc d = desc_of(a, s, mode);
+    const Desc d = desc_of(a, s, mode, p);
+    const bool ext = a.N > p;
     int kout[3] = {0, 0, 0};
     int nout = 2;
     if (d.cls == 0) { kout[0] = a.N; kout[1] = a.N + 1; }
@@ -155,12 +174,35 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
         }
         if (k <= a.N) wxor(Pa, L);
         if (k != a.N) {
-          int amt = ((k < a.N ? k : p) - d.base) % p;
-          if (amt < 0) amt += p;
-          rot_acc(acc, L, amt, p);
+          if (ext && k < a.N) {
+            add_coeff(acc, L, k, p);
+          } else {
+            int amt = ((k < a.N ? k : p) - d.base) % p;
+            if (amt < 0) amt += p;
+            rot_acc(acc, L, amt, p);
+          }
         }
       }
-      if (d.cls == 0) {
+      const ExtProg* pr = ext ? a.prog + static_cast<int64_t>(s) * a.prog_stride : nullptr;
+      if (ext && (d.cls == 1 || d.cls == 2 || d.cls == 3)) {  // extended code (Lemma 23.2 with Eq. (qext))
+        if (d.cls == 1) {
+          o[0] = Pa;
+          add_coeff(acc, Pa, d.x, p);
+          reduce(acc, p);
+          o[1] = acc;
+        } else if (d.cls == 2) {
+          reduce(acc, p);
+          mul_prog(acc, pr, p, o[0]);
+          o[1] = Pa;
+          wxor(o[1], o[0]);
+        } else {
+          add_coeff(acc, Pa, d.x, p);
+          reduce(acc, p);
+          mul_prog(acc, pr, p, o[1]);
+          o[0] = o[1];
+          wxor(o[0], Pa);
+        }
+      } else if (d.cls == 0) {
         o[0] = Pa;
         reduce(acc, p);
         o[1] = acc;

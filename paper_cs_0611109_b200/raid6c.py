@@ -38,6 +38,7 @@ _SIGS = [
     ("raid6c_parity_bytes", _sz, [_i, _sz]),
     ("raid6c_valid_p", _i, [_i]),
     ("raid6c_has_fast_path", _i, [_i]),
+    ("raid6c_ext_supported", _i, [_i]),
     ("raid6c_status_string", ctypes.c_char_p, [_i]),
     ("raid6c_last_cuda_error", ctypes.c_char_p, []),
     ("raid6c_launch_count", ctypes.c_uint64, []),
@@ -110,6 +111,11 @@ def valid_p(p: int) -> bool:
 
 def has_fast_path(p: int) -> bool:
     return bool(_lib.raid6c_has_fast_path(p))
+
+
+def ext_supported(p: int) -> bool:
+    """Theorem 25.3: p admits the extended code (up to 2p-1 data strips)."""
+    return bool(_lib.raid6c_ext_supported(p))
 
 
 def launch_count() -> int:

@@ -45,6 +45,14 @@ def test_valid_p_and_fast_set():
         assert R.has_fast_path(q)
 
 
+def test_ext_supported_matches_oracle():
+    """Theorem 25.3 check in the library (host code) vs the oracle's, for all p <= 257."""
+    for q in range(3, 258):
+        if R.valid_p(q):
+            assert R.ext_supported(q) == oracle.ext_condition(q), q
+    assert not R.ext_supported(9)
+
+
 def test_status_strings():
     for st in range(9):
         assert R._lib.raid6c_status_string(st)

@@ -201,7 +201,9 @@ def test_argument_errors_are_synchronous():
     with pytest.raises(R.Raid6Error, match="INVALID_P"):
         R.Plan(9, 3, 100)
     with pytest.raises(R.Raid6Error, match="INVALID_N"):
-        R.Plan(5, 6, 100)
+        R.Plan(5, 10, 100)  # N > 2p - 1
+    with pytest.raises(R.Raid6Error, match="INVALID_N"):
+        R.Plan(7, 8, 100)  # N > p but 7 fails Theorem 25.3
     with pytest.raises(R.Raid6Error, match="SIZE"):
         R.Plan(5, 2, 0)
     plan = R.Plan(5, 2, 16)

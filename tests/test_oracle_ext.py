@@ -139,3 +139,14 @@ def test_ext_recover_basic_agrees_with_section_4():
         oracle.recover(p, D, i, j, a, nbytes)
         oracle.recover_ext(p, D, i, j, b, nbytes)
         assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+@pytest.mark.parametrize("p", [5, 13, 17])
+def test_ext_coeff_matrices(p):
+    """g_k of Eq. (qext) equals S^k (k < p) and Id + S^{k-p+1} (k >= p), with S^k built by
+    repeated matrix multiplication (oracle_sylvester_power) -- two constructions agree."""
+    n = p - 1
+    I = np.eye(n, dtype=np.uint8)
+    for k in range(2 * p - 1):
+        expect = oracle.sylvester_power(p, k) if k < p else oracle.sylvester_power(p, k - p + 1) ^ I
+        np.testing.assert_array_equal(oracle.ext_coeff(p, k), expect)
