@@ -150,11 +150,15 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     c = CONFIGS[args.config]
-    p, N, S = c["p"], c["N"], args.stripes or c["stripes"]
+    p, N, S = c["p"], args.data_strips or c["N"], args.stripes or c["stripes"]
     nbytes = args.strip_bytes or c["nbytes"]
     if args.strip_bytes and not args.stripes and args.config == 3:  # c3 sweep: >= 4 GiB per point
         S = max(1, -(-(4 << 30) // (N * nbytes)))
-    c = dict(c, desc=c["desc"] if not args.strip_bytes else f"{c['desc']} [strip {nbytes} B, {S} stripes]")
+    if args.data_strips and not args.stripes:  # keep the batch's user data about the config's
+        S = max(1, (c["stripes"] * c["N"]) // N)
+    if args.strip_bytes or args.data_strips:
+        c = dict(c, desc=f"{c['desc']} [N={N}{' (extended code, Eq. qext)' if N > p else ''}, strip {nbytes} B, "
+                         f"{S} stripes]")
     pb = R.parity_bytes(p, nbytes)
     ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
     stripe0 = shard.weak_range(rank, S)[0]  # weak scaling: each rank owns distinct global stripes
@@ -298,7 +302,9 @@ def run_next1(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     c = CONFIGS[args.config]
-    p, N, S = c["p"], c["N"], args.stripes or c["stripes"]
+    p, N, S = c["p"], args.data_strips or c["N"], args.stripes or c["stripes"]
+    if args.data_strips and not args.stripes:
+        S = max(1, (c["stripes"] * c["N"]) // N)
     nbytes = args.strip_bytes or c["nbytes"]
     pb = R.parity_bytes(p, nbytes)
     ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
@@ -412,7 +418,7 @@ def oracle_sample_check(p, N, nbytes, cfg, sparse_mode, stripe0, par):
             if g0 == max(0, W // 8 - 2):
                 b1 = nbytes
             segs = [synthetic.strip_bytes(0, cfg, gs, k, nbytes, sparse, lo=b0, hi=b1) for k in range(N)]
-            P, Q = oracle.encode(p, segs, b1 - b0)
+            P, Q = (oracle.encode_ext if N > p else oracle.encode)(p, segs, b1 - b0)
             e = b0 + P.size
             ok &= bool(np.array_equal(par[s, 0, b0:e].cpu().numpy(), P))
             ok &= bool(np.array_equal(par[s, 1, b0:e].cpu().numpy(), Q))
@@ -440,7 +446,8 @@ def _oracle_work(p, N, nbytes, cfg, sparse_mode, budget_s, max_threads):
         data = [synthetic.strip_bytes(0, cfg, s, k, nbytes, sparse, lo=0, hi=sample_bytes) for k in range(N)]
         t0 = time.perf_counter()
         user = 0
-        P, Q = oracle.encode(p, data, sample_bytes)
+        ext = N > p
+        P, Q = (oracle.encode_ext if ext else oracle.encode)(p, data, sample_bytes)
         if ops != "rec":
             user += N * sample_bytes
         if ops != "enc":
@@ -448,7 +455,7 @@ def _oracle_work(p, N, nbytes, cfg, sparse_mode, budget_s, max_threads):
             strips = [d.copy() for d in data] + [P.copy(), Q.copy()]
             strips[i][:] = 0
             strips[j][:] = 0
-            oracle.recover(p, N, i, j, strips, sample_bytes)
+            (oracle.recover_ext if ext else oracle.recover)(p, N, i, j, strips, sample_bytes)
             user += N * sample_bytes
         return user, time.perf_counter() - t0
 
@@ -510,6 +517,8 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--stripes", type=int, default=0, help="override stripes per GPU per step")
     ap.add_argument("--strip-bytes", type=int, default=0, help="override strip length (c3 sweep)")
+    ap.add_argument("--data-strips", type=int, default=0,
+                    help="override N (p < N <= 2p-1 selects the extended code of Eq. (qext), NEXT-2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--op", default="step", choices=["step", "update", "scrub"],
                     help="step = encode + recover (the metric); update / scrub = NEXT-1 kernels")
