@@ -69,6 +69,14 @@ def _lib():
             lib.oracle_ext_coeff.argtypes = [i, i, u8p]
             lib.oracle_encode_ext.argtypes = [i, i, pp, sz, u8p, u8p]
             lib.oracle_recover_ext.argtypes = [i, i, i, i, pp, sz]
+            u8 = ctypes.c_uint8
+            for nm, res, args in [("oracle_rs_mul2", u8, [u8]), ("oracle_rs_mul", u8, [u8, u8]),
+                                  ("oracle_rs_exp", u8, [i]), ("oracle_rs_inv", u8, [u8])]:
+                f = getattr(lib, nm)
+                f.restype = res
+                f.argtypes = args
+            lib.oracle_rs_encode.argtypes = [i, pp, sz, u8p, u8p]
+            lib.oracle_rs_recover.argtypes = [i, i, i, pp, sz]
             _lib_handle = lib
     return _lib_handle
 
@@ -238,4 +246,40 @@ def recover_ext(p: int, D: int, lost_i: int, lost_j: int, strips, nbytes: int):
     rc = _lib().oracle_recover_ext(p, D, lost_i, lost_j, _ptr_array(strips), nbytes)
     if rc != 0:
         raise ValueError(f"oracle_recover_ext failed rc={rc} (p={p} D={D} lost=({lost_i},{lost_j}))")
+    return strips
+
+
+# ------------------------------------------------------ GF(256) Reed-Solomon (NEXT-3)
+def rs_mul2(x: int) -> int:
+    return int(_lib().oracle_rs_mul2(x))
+
+
+def rs_mul(a: int, b: int) -> int:
+    return int(_lib().oracle_rs_mul(a, b))
+
+
+def rs_exp(k: int) -> int:
+    return int(_lib().oracle_rs_exp(k))
+
+
+def rs_inv(a: int) -> int:
+    return int(_lib().oracle_rs_inv(a))
+
+
+def rs_encode(data, nbytes: int | None = None):
+    """Eq. (rsparity): returns (P, Q), each ``nbytes`` long."""
+    if nbytes is None:
+        nbytes = int(np.asarray(data[0]).size)
+    data = _as_strips(data, nbytes)
+    P = np.zeros(nbytes, np.uint8)
+    Q = np.zeros(nbytes, np.uint8)
+    if _lib().oracle_rs_encode(len(data), _ptr_array(data), nbytes, _p(P), _p(Q)) != 0:
+        raise ValueError("oracle_rs_encode: invalid arguments")
+    return P, Q
+
+
+def rs_recover(N: int, lost_i: int, lost_j: int, strips, nbytes: int):
+    assert len(strips) == N + 2
+    if _lib().oracle_rs_recover(N, lost_i, lost_j, _ptr_array(strips), nbytes) != 0:
+        raise ValueError("oracle_rs_recover failed")
     return strips

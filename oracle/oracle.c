@@ -615,3 +615,110 @@ int oracle_recover_ext(int p, int D, int lost_i, int lost_j, uint8_t *const *str
     free(G); free(A); free(M);
     return rc;
 }
+
+/* =====================================================================================
+ * NEXT-3: the paper's comparison system, Reed-Solomon RAID-6 over GF(2^8) ("DP-RAID"),
+ * Sec. 4.1-4.4: g = {02}, reduction polynomial x^8+x^4+x^3+x^2+1.
+ * Bytes are field elements (bit i = coefficient of x^i).
+ * ===================================================================================== */
+
+/* Multiplication by g = {02}: y = (x << 1) ^ ((x & 0x80) ? 0x1d : 0x00). */
+uint8_t oracle_rs_mul2(uint8_t x) { return (uint8_t)((uint8_t)(x << 1) ^ ((x & 0x80) ? 0x1d : 0x00)); }
+
+/* a * b in GF(2^8): b = sum_i b_i x^i, so a*b = sum_i b_i (g^i a) -- shift and add with mul2. */
+uint8_t oracle_rs_mul(uint8_t a, uint8_t b) {
+    uint8_t r = 0;
+    for (int i = 0; i < 8; i++) {
+        if ((b >> i) & 1) r ^= a;
+        a = oracle_rs_mul2(a);
+    }
+    return r;
+}
+
+/* g^k (k >= 0) by k multiplications by g. */
+uint8_t oracle_rs_exp(int k) {
+    uint8_t r = 1;
+    for (int i = 0; i < k; i++) r = oracle_rs_mul2(r);
+    return r;
+}
+
+/* a^{-1} by exhaustive search over the 255 nonzero field elements; 0 for a = 0. */
+uint8_t oracle_rs_inv(uint8_t a) {
+    for (int b = 1; b < 256; b++)
+        if (oracle_rs_mul(a, (uint8_t)b) == 1) return (uint8_t)b;
+    return 0;
+}
+
+/*
+ * Eq. (rsparity): P = D_0 + ... + D_{N-1}, Q = D_0 + g D_1 + ... + g^{N-1} D_{N-1},
+ * byte by byte, Q by Horner's rule Q = D_0 + g(D_1 + g(... + g D_{N-1})).
+ * 1 <= N <= 255 (g has order 255).  All strips `bytes` long (P, Q too).
+ */
+int oracle_rs_encode(int N, const uint8_t *const *strips, size_t bytes, uint8_t *P, uint8_t *Q) {
+    if (N < 1 || N > 255) return -1;
+    for (size_t b = 0; b < bytes; b++) {
+        uint8_t p = 0, q = strips[N - 1][b];
+        for (int i = 0; i < N; i++) p ^= strips[i][b];
+        for (int i = N - 2; i >= 0; i--) q = (uint8_t)(oracle_rs_mul2(q) ^ strips[i][b]);
+        P[b] = p;
+        Q[b] = q;
+    }
+    return 0;
+}
+
+/*
+ * Two-erasure recovery (strip indices 0..N-1 data, N = P, N+1 = Q):
+ *   (P, Q): re-encode;  (D_j, Q): D_j = P + sum_{k!=j} D_k, then Q;
+ *   (D_j, P): D_j = g^{-j}(Q + Q_j), Q_j = sum_{k!=j} g^k D_k (Lemma 23.2), then P;
+ *   (D_x, D_y): Sec. 4.3: P_xy, Q_xy with the lost disks zero,
+ *     A = (1 + g^{y-x})^{-1}, B = g^{-x}(1 + g^{y-x})^{-1}, D_y = A(P + P_xy) + B(Q + Q_xy),
+ *     D_x = D_y + (P + P_xy).  A and B are computed once per pair.
+ */
+int oracle_rs_recover(int N, int lost_i, int lost_j, uint8_t *const *strips, size_t bytes) {
+    if (N < 1 || N > 255) return -1;
+    if (lost_i == lost_j || lost_i < 0 || lost_j < 0 || lost_i >= N + 2 || lost_j >= N + 2) return -1;
+    int x = lost_i < lost_j ? lost_i : lost_j, y = lost_i < lost_j ? lost_j : lost_i;
+    const int iP = N, iQ = N + 1;
+    if (x == iP && y == iQ) return oracle_rs_encode(N, (const uint8_t *const *)strips, bytes, strips[iP], strips[iQ]);
+    if (y == iQ) {
+        for (size_t b = 0; b < bytes; b++) {
+            uint8_t v = strips[iP][b];
+            for (int k = 0; k < N; k++)
+                if (k != x) v ^= strips[k][b];
+            strips[x][b] = v;
+        }
+        uint8_t *Pd = (uint8_t *)malloc(bytes ? bytes : 1);
+        int rc = oracle_rs_encode(N, (const uint8_t *const *)strips, bytes, Pd, strips[iQ]);
+        free(Pd);
+        return rc;
+    }
+    if (y == iP) {
+        uint8_t ginv = oracle_rs_inv(oracle_rs_exp(x));
+        for (size_t b = 0; b < bytes; b++) {
+            uint8_t q = strips[iQ][b];
+            for (int k = 0; k < N; k++)
+                if (k != x) q ^= oracle_rs_mul(oracle_rs_exp(k), strips[k][b]);
+            uint8_t d = oracle_rs_mul(ginv, q);
+            strips[x][b] = d;
+            uint8_t p = d;
+            for (int k = 0; k < N; k++)
+                if (k != x) p ^= strips[k][b];
+            strips[iP][b] = p;
+        }
+        return 0;
+    }
+    uint8_t A = oracle_rs_inv((uint8_t)(1 ^ oracle_rs_exp(y - x)));
+    uint8_t B = oracle_rs_mul(oracle_rs_inv(oracle_rs_exp(x)), A);
+    for (size_t b = 0; b < bytes; b++) {
+        uint8_t dp = strips[iP][b], dq = strips[iQ][b];
+        for (int k = 0; k < N; k++) {
+            if (k == x || k == y) continue;
+            dp ^= strips[k][b];
+            dq ^= oracle_rs_mul(oracle_rs_exp(k), strips[k][b]);
+        }
+        uint8_t dy = (uint8_t)(oracle_rs_mul(A, dp) ^ oracle_rs_mul(B, dq));
+        strips[y][b] = dy;
+        strips[x][b] = (uint8_t)(dy ^ dp);
+    }
+    return 0;
+}
