@@ -150,25 +150,47 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     c = CONFIGS[args.config]
-    p, N, S = c["p"], args.data_strips or c["N"], args.stripes or c["stripes"]
+    p, N, S = args.prime or c["p"], args.data_strips or c["N"], args.stripes or c["stripes"]
     nbytes = args.strip_bytes or c["nbytes"]
     if args.strip_bytes and not args.stripes and args.config == 3:  # c3 sweep: >= 4 GiB per point
         S = max(1, -(-(4 << 30) // (N * nbytes)))
     if args.data_strips and not args.stripes:  # keep the batch's user data about the config's
         S = max(1, (c["stripes"] * c["N"]) // N)
-    if args.strip_bytes or args.data_strips:
-        c = dict(c, desc=f"{c['desc']} [N={N}{' (extended code, Eq. qext)' if N > p else ''}, strip {nbytes} B, "
+    if args.strip_bytes or args.data_strips or args.prime:
+        c = dict(c, desc=f"{c['desc']} [p={p} N={N}{' (extended code, Eq. qext)' if N > p else ''}, strip {nbytes} B, "
                          f"{S} stripes]")
-    pb = R.parity_bytes(p, nbytes)
+    rs = args.code == "rs"  # NEXT-3: the paper's GF(256) Reed-Solomon comparison system, same workload
+    pb = nbytes if rs else R.parity_bytes(p, nbytes)
     ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
+    if rs:
+        c = dict(c, desc=f"RS GF(256) baseline (Eq. rsparity) on {c['desc']}")
     stripe0 = shard.weak_range(rank, S)[0]  # weak scaling: each rank owns distinct global stripes
     stream = torch.cuda.Stream(device=dev)
     data = torch.empty((S, N, ss), dtype=torch.uint8, device=dev)
     par = torch.zeros((S, 2, ps), dtype=torch.uint8, device=dev)
     R.fill(data, ss, N * ss, nbytes, N, S, 0, args.config, stripe0, 0, c["sparse"], stream)
-    plan = R.Plan(p, N, nbytes, local, stream)
     a_data, a_par = int(data.data_ptr()), int(par.data_ptr())
     enc_args = (a_data, ss, N * ss, a_par, a_par + ps, 2 * ps, S)
+    if rs:
+        class _RSPlan:  # same call shape as Plan for the timed loop
+            def encode_strided(self, *a):
+                R.rs_encode_strided(N, nbytes, *a, stream=stream)
+
+            def recover_strided(self, *a):
+                R.rs_recover_strided(N, nbytes, *a[:-1], a[-1], stream=stream)
+
+            def sync(self):
+                stream.synchronize()
+
+            def close(self):
+                pass
+
+            def encode_host(self, *a):
+                raise NotImplementedError
+
+        plan = _RSPlan()
+    else:
+        plan = R.Plan(p, N, nbytes, local, stream)
     ops = c["ops"]
     do_enc = ops.startswith("enc")
     do_rec = ops != "enc"
@@ -234,14 +256,15 @@ def run_ours(args):
         checked = 2 * data.numel() if do_rec else 0
         oracle_ok = None
         if rank == 0 and args.oracle_check:
-            oracle_ok = oracle_sample_check(p, N, nbytes, args.config, c["sparse"], stripe0, par)
+            oracle_ok = (rs_sample_check if rs else oracle_sample_check)(p, N, nbytes, args.config, c["sparse"],
+                                                                        stripe0, par)
         tot = shard.sum_over_ranks([mism, checked], dev)
         verified = {"mismatched_bytes": tot[0], "checked_bytes": tot[1], "oracle_segments_match": oracle_ok}
         del ref_data, ref_par
 
     # ---------------------------------------------------------------- e2e (host buffers, public API)
     e2e = None
-    if args.e2e and do_enc:
+    if args.e2e and do_enc and not rs:
         e2e = run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_lists, do_rec, world, dev)
 
     user_bytes_step = (int(do_enc) + int(do_rec)) * N * nbytes * S
@@ -259,7 +282,8 @@ def run_ours(args):
     dom = max(kern, key=lambda k: k[2])
     traffic = traffic_from_profile(args.config)
     roof = {
-        "kernel": f"zp_kernel<{p},{'true' if dom[0] == 'recover' else 'false'}> ({dom[0]})",
+        "kernel": (f"rs_kernel<{'true' if dom[0] == 'recover' else 'false'}> ({dom[0]})" if rs else
+                   f"zp_kernel<{p},{1 if dom[0] == 'recover' else 0}> ({dom[0]})"),
         "bound": "hbm", "achieved": round(dom[1] / (dom[2] / 1e3) / 1e9, 1), "peak": peak, "unit": "GB/s",
         "frac": round(dom[1] / (dom[2] / 1e3) / 1e9 / peak, 4), "peak_source": peak_src,
         "traffic": traffic.get(dom[0]) if isinstance(traffic, dict) else None,
@@ -280,9 +304,9 @@ def run_ours(args):
                    "l2": "working set >= 1 GiB >> 126 MB L2 (no flush needed)"},
         "roofline": roof, "kernels": per_kernel, "gpu_launches": launches, "clocks": clk,
         "verified": verified, "e2e": e2e,
-        "fast_path": R.has_fast_path(p),
+        "fast_path": R.has_fast_path(p), "code": args.code,
     }
-    if rank == 0 and world == 1 and args.cpu_baseline:  # the oracle baseline: rank 0 at N=1 only
+    if rank == 0 and world == 1 and args.cpu_baseline and not rs:  # the oracle baseline: rank 0 at N=1 only
         line["cpu_baseline"] = cpu_baseline(args, p, N, nbytes, args.config, c["sparse"])
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -401,6 +425,24 @@ def run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_list
             "matches_device_path": same}
 
 
+def rs_sample_check(p, N, nbytes, cfg, sparse_mode, stripe0, par):
+    """RS baseline: sampled byte segments of P/Q of two stripes against oracle.rs_encode."""
+    import numpy as np
+    import oracle
+    import synthetic
+    ok = True
+    for s in (0, par.shape[0] - 1):
+        gs = stripe0 + s
+        sparse = sparse_mode == 1 or (sparse_mode == 2 and gs % 2 == 1)
+        for b0 in (0, nbytes // 2, max(0, nbytes - 4096)):
+            b1 = min(nbytes, b0 + 4096)
+            segs = [synthetic.strip_bytes(0, cfg, gs, k, nbytes, sparse, lo=b0, hi=b1) for k in range(N)]
+            P, Q = oracle.rs_encode(segs, b1 - b0)
+            ok &= bool(np.array_equal(par[s, 0, b0:b1].cpu().numpy(), P))
+            ok &= bool(np.array_equal(par[s, 1, b0:b1].cpu().numpy(), Q))
+    return ok
+
+
 def oracle_sample_check(p, N, nbytes, cfg, sparse_mode, stripe0, par):
     """Sampled word-aligned P/Q segments of two stripes against the CPU oracle."""
     import numpy as np
@@ -517,9 +559,12 @@ def main():
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--stripes", type=int, default=0, help="override stripes per GPU per step")
     ap.add_argument("--strip-bytes", type=int, default=0, help="override strip length (c3 sweep)")
+    ap.add_argument("--prime", type=int, default=0, help="override p (e.g. 17 for the paper's Z_17)")
     ap.add_argument("--data-strips", type=int, default=0,
                     help="override N (p < N <= 2p-1 selects the extended code of Eq. (qext), NEXT-2)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--code", default="zp", choices=["zp", "rs"],
+                    help="zp = the paper's Z_p code (default); rs = its GF(256) RS comparison system (NEXT-3)")
     ap.add_argument("--op", default="step", choices=["step", "update", "scrub"],
                     help="step = encode + recover (the metric); update / scrub = NEXT-1 kernels")
     ap.add_argument("--no-verify", dest="verify", action="store_false")

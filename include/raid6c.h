@@ -175,6 +175,22 @@ raid6c_status raid6c_update_strided(raid6c_plan plan, uint8_t *data, size_t stri
                                     size_t new_stride, const int32_t *disks, int num_disks,
                                     int disks_on_device);
 
+/* ------------------------------------------------ comparison system */
+
+/* The paper's comparison system, Reed-Solomon RAID-6 over GF(2^8) (Sec. 4.1-4.4,
+ * PAPER.md:818-1039): P = sum D_i, Q = sum g^i D_i with g = {02} and reduction polynomial
+ * x^8+x^4+x^3+x^2+1 (Eq. (rsparity)); recovery per Sec. 4.3.  1 <= N <= 255 data strips; every
+ * strip (data, P, Q) is `bytes` long.  Same layout, pointer and error conventions as the
+ * strided Z_p calls; stream-ordered on `stream` (a cudaStream_t, NULL = legacy default). */
+raid6c_status raid6c_rs_encode_strided(int N, size_t bytes, const uint8_t *data, size_t strip_stride,
+                                       size_t stripe_stride, uint8_t *P, uint8_t *Q,
+                                       size_t parity_stride, int num_stripes, void *stream);
+raid6c_status raid6c_rs_recover_strided(int N, size_t bytes, uint8_t *data, size_t strip_stride,
+                                        size_t stripe_stride, uint8_t *P, uint8_t *Q,
+                                        size_t parity_stride, int num_stripes,
+                                        const raid6c_erasure *erasures, int num_erasures,
+                                        int erasures_on_device, void *stream);
+
 /* ------------------------------------------------ host-buffer calls (end-to-end path) */
 
 /* Same as the strided calls, but every pointer is HOST memory (pinned memory gives

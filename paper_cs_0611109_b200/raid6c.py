@@ -52,6 +52,8 @@ _SIGS = [
     ("raid6c_recover_strided", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _i, _i]),
     ("raid6c_scrub_strided", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp]),
     ("raid6c_update_strided", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _sz, _vp, _i, _i]),
+    ("raid6c_rs_encode_strided", _i, [_i, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp]),
+    ("raid6c_rs_recover_strided", _i, [_i, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _i, _i, _vp]),
     ("raid6c_encode_host", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i]),
     ("raid6c_recover_host", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _i]),
     ("raid6c_host_traffic", _i, [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
@@ -151,6 +153,25 @@ def fill(dst, strip_stride: int, stripe_stride: int, nbytes: int, nstrips: int, 
 def count_mismatch(a, b, nbytes: int, count_dev, stream=None) -> None:
     _check(_lib.raid6c_count_mismatch(_ptr(a), _ptr(b), nbytes, _ptr(count_dev), _stream_handle(stream)),
            "raid6c_count_mismatch")
+
+
+# ------------------------------------------------------------------ NEXT-3: RS baseline
+def rs_encode_strided(N, nbytes, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, stream=None):
+    _check(_lib.raid6c_rs_encode_strided(N, nbytes, _ptr(data), strip_stride, stripe_stride, _ptr(P), _ptr(Q),
+                                         parity_stride, num_stripes, _stream_handle(stream)), "raid6c_rs_encode_strided")
+
+
+def rs_recover_strided(N, nbytes, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, erasures,
+                       stream=None):
+    if hasattr(erasures, "is_cuda") and erasures.is_cuda:
+        _check(_lib.raid6c_rs_recover_strided(N, nbytes, _ptr(data), strip_stride, stripe_stride, _ptr(P), _ptr(Q),
+                                              parity_stride, num_stripes, _ptr(erasures), erasures.shape[0], 1,
+                                              _stream_handle(stream)), "raid6c_rs_recover_strided")
+    else:
+        arr = _erasure_array(erasures)
+        _check(_lib.raid6c_rs_recover_strided(N, nbytes, _ptr(data), strip_stride, stripe_stride, _ptr(P), _ptr(Q),
+                                              parity_stride, num_stripes, ctypes.cast(arr, _vp), len(arr), 0,
+                                              _stream_handle(stream)), "raid6c_rs_recover_strided")
 
 
 # ------------------------------------------------------------------ plans
