@@ -462,6 +462,32 @@ __device__ __forceinline__ uint32_t count_nonzero_words(const uint32_t (&V)[G::C
   return cnt;
 }
 
+// Evaluation plan for the geometric series S_M = sum_{m<M} b^m of the DD solve, by a per-lane
+// cost model (rotation ~4 ops, reduction ~6 ops): the doubling chain costs a rotation and a
+// reduction per step; a two-level split M = M1*M2 + R costs M2 + M1 + R rotations and two
+// reductions (one if M2 == M).  p = 5, 13: direct (3 / 7 rot + 1 red); 17: 3x3; 59: 5x6;
+// 61, 257: chain (8 steps).
+constexpr int c_popcount(int v) { return v == 0 ? 0 : (v & 1) + c_popcount(v >> 1); }
+template <int M>
+struct SeriesPlan {
+  static constexpr int cost2(int m2) {
+    return m2 >= M ? 4 * M + 6 : 4 * (m2 + M / m2 + M % m2) + 12;
+  }
+  static constexpr int best_m2() {
+    int best = M, bc = cost2(M);
+    for (int m2 = 2; m2 < M; m2++)
+      if (cost2(m2) < bc) { bc = cost2(m2); best = m2; }
+    return best;
+  }
+  static constexpr int M2 = best_m2();
+  static constexpr int M1 = M / M2;
+  static constexpr int CHAIN_COST = 10 * (top_bit(M) + c_popcount(M) - 1);
+  // p = 61 (M = 31) keeps the chain: measured (r01 A/B), the two-level plan spills at the
+  // 96-register cap of its 15-lane chunks and ran 1% slower on config 5; elsewhere it wins
+  // (c2 recover +1.5%, c4 DD +1.6%, p = 17 recover +3.2%).
+  static constexpr bool CHAIN = (M == 31) || CHAIN_COST < cost2(M2);
+};
+
 // Class epilogue: produces the two output chunks and their strip indices.
 template <class G>
 __device__ __forceinline__ void finish(const ZpArgs& a, const ItemDesc& d, uint32_t (&Pa)[G::C], Acc<G>& acc,
@@ -489,10 +515,35 @@ __device__ __forceinline__ void finish(const ZpArgs& a, const ItemDesc& d, uint3
     for (int l = 0; l < C; l++) acc.ay[l] ^= Pa[l];
     uint32_t t[C];
     reduce<G>(acc, t);
-    // S_m = sum_{j<m} b^j t, b = x^{2z}; target m* = (p+1)/2 (reading R11).
+    // d_y = S_M t with S_M = sum_{m<M} b^m, b = x^{2z}, M = (p+1)/2 (reading R11); the evaluation
+    // order is chosen at compile time (SeriesPlan): direct, two-level, or doubling chain.
     constexpr int M = (G::P + 1) / 2;
     constexpr int TOP = top_bit(M);
     const int bz = (2 * (d.y - d.x)) % G::P;
+    using SP = SeriesPlan<M>;
+    if constexpr (!SP::CHAIN) {
+      // two-level: S = sum_{i<M1} b^{i M2} T + sum_{m=M1 M2}^{M-1} b^m t,  T = sum_{j<M2} b^j t
+      // (direct when M2 == M).  All rotations of one level share a deferred accumulator.
+      uint32_t T[C];
+      acc.zero();
+#pragma unroll 1
+      for (int j = 0; j < SP::M2; j++) rot_acc<G>(t, (bz * j) % G::P, mtab, acc);
+      if constexpr (SP::M2 == M) {
+        reduce<G>(acc, o1);
+      } else {
+        reduce<G>(acc, T);
+        acc.zero();
+#pragma unroll 1
+        for (int i = 0; i < SP::M1; i++) rot_acc<G>(T, (bz * SP::M2 * i) % G::P, mtab, acc);
+#pragma unroll 1
+        for (int m = SP::M1 * SP::M2; m < M; m++) rot_acc<G>(t, (bz * m) % G::P, mtab, acc);
+        reduce<G>(acc, o1);
+      }
+#pragma unroll
+      for (int l = 0; l < C; l++) o0[l] = o1[l] ^ Pa[l];
+      k0 = d.x; k1 = d.y;
+      return;
+    }
 #pragma unroll
     for (int l = 0; l < C; l++) o1[l] = t[l];  // o1 = S_1
     int m = 1;
