@@ -145,10 +145,14 @@ def run_ours(args):
     from paper_cs_0611109_b200 import shard
 
     rank, world, local = _env_rank()
+    local = local % torch.cuda.device_count()  # (only differs in the 1-GPU multi-rank rehearsal)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # gloo: rehearse the multi-rank path with several ranks on one GPU (host-side collectives only)
+            dist.init_process_group("gloo")
     c = CONFIGS[args.config]
     p, N, S = args.prime or c["p"], args.data_strips or c["N"], args.stripes or c["stripes"]
     nbytes = args.strip_bytes or c["nbytes"]
@@ -393,7 +397,7 @@ def run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_list
     H2D of inputs and D2H of results inside the timed region, pinned host memory."""
     hd = torch.empty((S, N, ss), dtype=torch.uint8).pin_memory()
     hp = torch.zeros((S, 2, ps), dtype=torch.uint8).pin_memory()
-    hd.copy_(data.cpu())
+    hd.copy_(data)  # device -> pinned host, no pageable temporary
     hd_ptr, hp_ptr = int(hd.data_ptr()), int(hp.data_ptr())
     a = (hd_ptr, ss, N * ss, hp_ptr, hp_ptr + ps, 2 * ps, S)
     steps = max(1, args.e2e_steps)
@@ -574,6 +578,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--cpu-threads", type=int, default=64)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: rehearse N>1 on fewer GPUs (ranks share devices; timing not meaningful)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warm-up raised to 3 (timing rule)", file=sys.stderr)

@@ -24,9 +24,15 @@ def max_over_ranks(value: float, device=None) -> float:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def _coll_device(device):
+    """NCCL reduces device tensors; gloo (CPU tests, 1-GPU rehearsal) reduces host tensors."""
+    import torch.distributed as dist
+    return device if dist.get_backend() == "nccl" else "cpu"
 
 
 def sum_over_ranks(values, device=None) -> list[int]:
@@ -35,6 +41,6 @@ def sum_over_ranks(values, device=None) -> list[int]:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return [int(v) for v in values]
-    t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=device)
+    t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return [int(v) for v in t.tolist()]
