@@ -66,3 +66,17 @@ def test_no_device_is_reported_not_faked():
         R.Plan(13, 12, 4096)
     with pytest.raises(R.Raid6Error):
         R.encode(13, 1, [0], 0, 0, 16)  # NULL pointers are rejected before any device call
+
+
+def test_build_and_shard_import_without_library():
+    """A fresh checkout has no libraid6c.so: the build module (which makes it) and the host
+    sharding logic must import, while the binding itself must fail loudly (no fallback)."""
+    import sys
+    env = dict(os.environ, RAID6C_LIB="/nonexistent/libraid6c.so")
+    code = ("import paper_cs_0611109_b200.build, paper_cs_0611109_b200.shard\n"
+            "try:\n"
+            "    from paper_cs_0611109_b200 import raid6c\n"
+            "except ImportError as e:\n"
+            "    assert 'no CPU fallback' in str(e); print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr
