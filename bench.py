@@ -320,6 +320,205 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+FULL_STRIPES = {2: 256, 4: 4096, 5: 1000}  # BASELINE.json configs[1], [3], [4]: whole-config stripe counts
+
+
+def run_full(args):
+    """--full: the whole configuration, not one resident batch.
+
+    The config's S stripes (c4: 4096, c5: 1000, c2: 256) are block-partitioned over the ranks
+    (strong scaling: rank r owns [floor(r*S/G), floor((r+1)*S/G))), and each rank streams its
+    block through one resident wave buffer (c4: 64 x 58 x 8 MiB, c5: 16 x 60 x 32 MiB), allocated
+    once.  Per wave: generate on device (untimed), encode (timed, except c5 where parity is only
+    the recovery's input), poison the wave's lost strips (untimed), recover them in place (timed),
+    scrub the wave (untimed).  The scrub proves every recovery: with the N surviving strips given,
+    the lost pair is the unique solution of both parity equations (Lemma 23.2),
+    so a stripe with zero violating words after recovery was rebuilt exactly.  Sampled P/Q
+    segments are compared with the CPU oracle.  value = user bytes of all ranks / max-rank sum of
+    the timed kernel intervals (CUDA events on the plan's stream)."""
+    import torch
+    import torch.distributed as dist
+    import synthetic
+    from paper_cs_0611109_b200 import raid6c as R
+    from paper_cs_0611109_b200 import shard
+
+    rank, world, local = _env_rank()
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    if args.config not in FULL_STRIPES:
+        raise SystemExit(f"--full applies to configs {sorted(FULL_STRIPES)}")
+    c = CONFIGS[args.config]
+    p, N, nbytes = c["p"], c["N"], c["nbytes"]
+    total = args.stripes or FULL_STRIPES[args.config]
+    lo, hi = shard.block_range(rank, world, total)
+    wave = min(c["stripes"], max(1, hi - lo))
+    pb = R.parity_bytes(p, nbytes)
+    ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
+    stream = torch.cuda.Stream(device=dev)
+    data = torch.empty((wave, N, ss), dtype=torch.uint8, device=dev)
+    par = torch.zeros((wave, 2, ps), dtype=torch.uint8, device=dev)
+    counts = torch.zeros(wave, dtype=torch.int32, device=dev)
+    bad_total = torch.zeros(1, dtype=torch.int64, device=dev)
+    plan = R.Plan(p, N, nbytes, local, stream)
+    a_data, a_par = int(data.data_ptr()), int(par.data_ptr())
+    do_enc = c["ops"] != "rec"
+    flat_d, flat_p = data.view(wave * N, ss), par.view(wave * 2, ps)
+
+    def wave_tables(w0, n):
+        """Erasure pairs and poison row indices of one wave, uploaded once before timing and kept
+        alive for the whole run (they are read on `stream` long after the host moves on)."""
+        pairs = pair_schedule(args.config, N, n, w0, 0)
+        dl = [s * N + k for s, pr in enumerate(pairs) for k in pr if k < N]
+        pl = [s * 2 + (k - N) for s, pr in enumerate(pairs) for k in pr if k >= N]
+        return (w0, n, pairs, torch.tensor(pairs, dtype=torch.int32, device=dev),
+                torch.tensor(dl, dtype=torch.int64, device=dev), torch.tensor(pl, dtype=torch.int64, device=dev))
+
+    tables = [wave_tables(w0, min(wave, hi - w0)) for w0 in range(lo, hi, wave)]
+    torch.cuda.synchronize(dev)
+
+    def run_wave(tab):
+        """One wave (fill, encode, poison, recover, scrub) on `stream`; returns its events."""
+        w0, n, pairs, pair_dev, dl, pl = tab
+        args_ = (a_data, ss, N * ss, a_par, a_par + ps, 2 * ps, n)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        with torch.cuda.stream(stream):
+            R.fill(data, ss, N * ss, nbytes, N, n, 0, args.config, w0, 0, c["sparse"], stream)
+            e[0].record(stream)
+            plan.encode_strided(*args_)
+            e[1].record(stream)
+            if dl.numel():
+                flat_d.index_fill_(0, dl, 0xA5)  # lost strips: never read by recovery
+            if pl.numel():
+                flat_p.index_fill_(0, pl, 0xA5)
+            e[2].record(stream)
+            plan.recover_strided(*args_, pair_dev)
+            e[3].record(stream)
+            plan.scrub_strided(*args_, counts)
+            bad_total.add_(counts[:n].sum())
+        return e
+
+    for _ in range(args.warmup):  # warm-up on the first wave (not counted)
+        run_wave(tables[0])
+    stream.synchronize()
+    bad_total.zero_()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = R.launch_count()
+    wall0 = time.perf_counter()
+    evs, classes, nst = [], {}, 0
+    for tab in tables:
+        evs.append(run_wave(tab))
+        nst += tab[1]
+        for (i, j) in tab[2]:
+            k = synthetic.pair_class(N, i, j)
+            classes[k] = classes.get(k, 0) + 1
+    stream.synchronize()
+    wall = time.perf_counter() - wall0
+    launches = R.launch_count() - launches0
+    clk = clocks.stop()
+    enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs) if do_enc else 0.0
+    rec_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
+    timed_ms = enc_ms + rec_ms
+    oracle_ok = None
+    if rank == 0 and args.oracle_check:
+        last_w0 = lo + ((hi - lo - 1) // wave) * wave
+        oracle_ok = oracle_sample_check(p, N, nbytes, args.config, c["sparse"], last_w0,
+                                        par[:min(wave, hi - last_w0)])
+    bad = int(bad_total.item())
+    t_max = shard.max_over_ranks(timed_ms, dev)
+    enc_max = shard.max_over_ranks(enc_ms, dev)
+    rec_max = shard.max_over_ranks(rec_ms, dev)
+    tot = shard.sum_over_ranks([nst, bad] + [classes.get(k, 0) for k in ("DD", "DP", "DQ", "PQ")], dev)
+    nst_all, bad_all = tot[0], tot[1]
+    ops_n = int(do_enc) + 1
+    user = ops_n * N * nbytes * nst_all
+    value = user / (t_max / 1e3) / 1e9
+    peak, peak_src = measured_peak()
+    per = {}
+    if do_enc:
+        per["encode"] = enc_max
+    per["recover"] = rec_max
+    kern = {k: {"alg_bytes_per_rank": nst * (N * nbytes + 2 * pb), "sum_ms_max_rank": round(v, 3),
+                "achieved_GBps_per_gpu": round(nst * (N * nbytes + 2 * pb) / (v / 1e3) / 1e9, 1),
+                "frac_of_peak": round(nst * (N * nbytes + 2 * pb) / (v / 1e3) / 1e9 / peak, 4),
+                "user_GBps_all_gpus": round(N * nbytes * nst_all / (v / 1e3) / 1e9, 1)} for k, v in per.items()}
+    dom = max(per, key=per.get)
+    ach = nst * (N * nbytes + 2 * pb) / (per[dom] / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": 1,
+        "warmup": args.warmup, "ms_per_step": round(t_max, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u32 (bitwise GF(2) words)",
+        "data": "synthetic (seeded SplitMix64 counter generator, generated on device per wave, untimed)",
+        "config": {"workload": f"c{args.config} full: {total} stripes of p={p} N={N} {nbytes} B strips, "
+                               f"block-sharded over {world} GPU(s), waves of {wave} ({c['ops']})",
+                   "p": p, "N": N, "strip_bytes": nbytes, "parity_bytes": pb, "stripes_total": total,
+                   "stripes_this_rank0": hi - lo if rank == 0 else None, "wave": wave, "ops": c["ops"],
+                   "parallelism": f"stripe-sharded x{world} (no data-path collective)",
+                   "l2": "each wave >= 30 GiB >> 126 MB L2 (no flush needed)",
+                   "timed": "sum of per-wave encode + recover kernel intervals; generation, poisoning, scrub untimed"},
+        "roofline": {"kernel": f"zp_kernel<{p},{1 if dom == 'recover' else 0}> ({dom})", "bound": "hbm",
+                     "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
+                     "peak_source": peak_src},
+        "kernels": kern, "gpu_launches": launches, "clocks": clk, "wall_s_rank0": round(wall, 2),
+        "classes": dict(zip(("DD", "DP", "DQ", "PQ"), tot[2:])),
+        "verified": {"stripes": nst_all, "scrub_bad_words_after_recovery": bad_all,
+                     "oracle_segments_match": oracle_ok},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_sweep(args):
+    """--sweep (config 3, BASELINE.json configs[2]): encode-only write-throughput sweep over strip
+    sizes 64 KiB -> 16 MiB (x2 steps, 9 points), each point >= 4 GiB of user data
+    (ceil(4 GiB / (64 * strip)) stripes).  Each point is a separate `bench.py --strip-bytes B`
+    process (so every point gets a fresh allocator); one JSON line collects them."""
+    rank, world, _ = _env_rank()
+    if world > 1:
+        raise SystemExit("--sweep is a 1-GPU measurement")
+    pts = []
+    for k in range(9):
+        b = (64 << 10) << k
+        cmd = [sys.executable, os.path.abspath(__file__), "--config", "3", "--strip-bytes", str(b),
+               "--steps", str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise SystemExit(f"sweep point {b} failed:\n{r.stderr[-2000:]}")
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        kk = d["kernels"]["encode"]
+        pts.append({"strip_bytes": b, "stripes": d["config"]["stripes_per_gpu"], "user_GBps": kk["user_GBps"],
+                    "achieved_GBps": kk["achieved_GBps"], "frac_of_peak": kk["frac_of_peak"],
+                    "avg_ms": kk["avg_ms"], "verified_oracle": d["verified"]["oracle_segments_match"],
+                    "clocks": d["clocks"]})
+    peak, peak_src = measured_peak()
+    best = max(pts, key=lambda q: q["achieved_GBps"])
+    worst = min(pts, key=lambda q: q["achieved_GBps"])
+    line = {"metric": METRIC + " (c3 encode write-throughput sweep)", "value": worst["user_GBps"], "unit": "GB/s",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32 (bitwise GF(2) words)", "data": "synthetic (device generator)",
+            "config": {"workload": "c3 sweep: p=257 N=64, strip 64 KiB -> 16 MiB, >= 4 GiB user data per point",
+                       "value_is": "the minimum user GB/s over the sweep points"},
+            "roofline": {"bound": "hbm", "achieved": worst["achieved_GBps"], "peak": peak, "unit": "GB/s",
+                         "frac": round(worst["achieved_GBps"] / peak, 4), "peak_source": peak_src,
+                         "best_frac": round(best["achieved_GBps"] / peak, 4)},
+            "sweep": pts}
+    print(json.dumps(line), flush=True)
+
+
 def run_next1(args):
     """--op update | scrub (NEXT-1): small-write parity update and scrub of the
     config's stripes, one launch per step, CUDA events on the plan's stream."""
@@ -571,6 +770,10 @@ def main():
                     help="zp = the paper's Z_p code (default); rs = its GF(256) RS comparison system (NEXT-3)")
     ap.add_argument("--op", default="step", choices=["step", "update", "scrub"],
                     help="step = encode + recover (the metric); update / scrub = NEXT-1 kernels")
+    ap.add_argument("--full", action="store_true",
+                    help="whole config (c4: 4096, c5: 1000, c2: 256 stripes) block-sharded over the ranks, "
+                         "streamed in waves (strong scaling); --stripes overrides the total")
+    ap.add_argument("--sweep", action="store_true", help="config 3 strip-size sweep 64 KiB -> 16 MiB")
     ap.add_argument("--no-verify", dest="verify", action="store_false")
     ap.add_argument("--no-oracle-check", dest="oracle_check", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
@@ -588,6 +791,10 @@ def main():
         run_reference(args)
     elif args.op != "step":
         run_next1(args)
+    elif args.full:
+        run_full(args)
+    elif args.sweep:
+        run_sweep(args)
     else:
         run_ours(args)
 
