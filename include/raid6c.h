@@ -191,6 +191,84 @@ raid6c_status raid6c_rs_recover_strided(int N, size_t bytes, uint8_t *data, size
                                         const raid6c_erasure *erasures, int num_erasures,
                                         int erasures_on_device, void *stream);
 
+/* ------------------------------------ cross-GPU stripe layout */
+
+/* The strips of one stripe may live on different GPUs ("ranks"): rank r holds the strips
+ * with global index in a contiguous range [k_lo, k_hi) of 0..N+1.  Both parity equations of
+ * Eq. (znparity) are sums over disks, and the reduction pi of
+ * R' = F2[x]/(x^p+1) -> R_p is a ring homomorphism (Eq. (powers)), so the
+ * syndromes split into per-rank partial sums of already-reduced words, and the recovery
+ * syndromes of Eq. (PQxy) likewise:
+ *
+ *   dP = sum_r dP_r,   dQ = sum_r dQ_r,   dP_r, dQ_r = the surviving strips of rank r only.
+ *
+ * A step is two launches per rank with a cross-rank barrier between them:
+ *   1. raid6c_partial_strided: rank r folds its local surviving strips into (dP_r, dQ_r)
+ *      (HBM-bound, the same TMA pipeline as encode) and stores word range g of the result
+ *      into part_p[g] / part_q[g] -- a slot owned by rank g, local or a peer pointer
+ *      (NVLink stores, overlapped with the fold tile by tile).
+ *   2. raid6c_combine_strided: rank g XORs the num_sources partial slots of its word range
+ *      (local memory, or peer pointers to pull from) and applies the class solve of
+ *      Lemma 23.2 / Sec. 4.6 in the same kernel, writing the
+ *      rebuilt strips (or P and Q for an encode) straight to their owners (peer pointers).
+ *
+ * Encode is the PQ case: pass erasures == NULL.  Word ranges: the parity-format strip
+ * (parity_bytes) is cut into ranges of raid6c_xgpu_range_bytes(p, bytes, G) bytes, range g =
+ * [g*range_bytes, min((g+1)*range_bytes, parity_bytes)); a range is a whole number of kernel
+ * tiles, so no tile straddles two owners.  Every pointer below is a DEVICE address valid on
+ * the plan's device (its own memory, or peer memory mapped with raid6c_ipc_open / peer
+ * access).  The two launches never wait on each other inside a kernel: ordering across
+ * ranks is the caller's barrier (stream-ordered collective or host barrier). */
+
+#define RAID6C_MAX_RANKS 64
+
+/* Word-range size for num_ranks owners of (p, bytes) stripes: a multiple of p's kernel tile
+ * (fast path) or byte group (generic path) such that num_ranks ranges cover parity_bytes.
+ * Host only.  0 on bad input. */
+size_t raid6c_xgpu_range_bytes(int p, size_t bytes, int num_ranks);
+
+/* Partial syndromes of the local strips.  strips: HOST array of N+2 DEVICE pointers indexed
+ * by global strip index; only [k_lo, k_hi) are read (others may be NULL).  Strip k of stripe
+ * s is at strips[k] + s*(k < N ? data_stride : parity_stride).  erasures: as in
+ * raid6c_recover_strided (host or device array of 1 or num_stripes pairs), or NULL for an
+ * encode.  Lost strips are not read.  Output for stripe s, word range g (bytes
+ * [g*range_bytes, ...) of the parity-format strip):
+ *   part_p[g] + s*part_stride + (off - g*range_bytes) <- dP_r bytes at offset off
+ *   part_q[g] + ...                                     <- dQ_r (reduced, rotation origin at
+ *                                                          the lost strip for DP/DD)
+ * part_p / part_q: HOST arrays of num_ranges DEVICE pointers; range_bytes from
+ * raid6c_xgpu_range_bytes(p, bytes, num_ranges); part_stride >= range_bytes when num_stripes > 1.
+ * Stream-ordered on the plan's stream. */
+raid6c_status raid6c_partial_strided(raid6c_plan plan, const uint8_t *const *strips, size_t data_stride,
+                                     size_t parity_stride, int num_stripes, const raid6c_erasure *erasures,
+                                     int num_erasures, int erasures_on_device, int k_lo, int k_hi,
+                                     int num_ranges, uint8_t *const *part_p, uint8_t *const *part_q,
+                                     size_t part_stride, size_t range_bytes);
+
+/* Combine + solve for bytes [range_lo, range_hi) of every stripe (range_lo a multiple of the
+ * range size; range_hi <= parity_bytes).  src_p / src_q: HOST arrays of num_sources DEVICE
+ * pointers; source r holds stripe s's partial of this range at src_p[r] + s*part_stride.
+ * strips: HOST array of N+2 DEVICE pointers (global index, strides as in the partial call);
+ * only the two output strips of each stripe are written (lost strips; P and Q for an
+ * encode), clipped to their length (`bytes` for data, parity_bytes for P/Q).  erasures must
+ * equal the partial call's.  Stream-ordered on the plan's stream. */
+raid6c_status raid6c_combine_strided(raid6c_plan plan, uint8_t *const *strips, size_t data_stride,
+                                     size_t parity_stride, int num_stripes, const raid6c_erasure *erasures,
+                                     int num_erasures, int erasures_on_device, int num_sources,
+                                     const uint8_t *const *src_p, const uint8_t *const *src_q,
+                                     size_t part_stride, size_t range_lo, size_t range_hi);
+
+/* Inter-process device memory for the cross-GPU layout (one process per GPU).
+ * raid6c_dev_alloc: cudaMalloc'd buffer on `device` (exportable; freed by raid6c_dev_free).
+ * raid6c_ipc_export: 64-byte CUDA IPC handle of a buffer from raid6c_dev_alloc.
+ * raid6c_ipc_open: map a peer's handle into this process on `device` (enables peer access
+ * to the owning device when it differs); close with raid6c_ipc_close. */
+raid6c_status raid6c_dev_alloc(size_t bytes, int device, void **dev_ptr);
+raid6c_status raid6c_dev_free(void *dev_ptr);
+raid6c_status raid6c_ipc_export(const void *dev_ptr, uint8_t handle[64]);
+raid6c_status raid6c_ipc_open(const uint8_t handle[64], int device, void **dev_ptr);
+raid6c_status raid6c_ipc_close(void *dev_ptr);
+
 /* ------------------------------------------------ host-buffer calls (end-to-end path) */
 
 /* Same as the strided calls, but every pointer is HOST memory (pinned memory gives

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <numeric>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -218,8 +219,8 @@ struct raid6c_plan_s {
   cudaStream_t stream = nullptr;
   const zp::FastEntry* fe = nullptr;
   int num_sms = 148;
-  int occ[4] = {1, 1, 1, 1};  // CTAs per SM per kernel mode
-  int occ_ext[4] = {1, 1, 1, 1};
+  int occ[5] = {1, 1, 1, 1, 1};  // CTAs per SM per kernel mode
+  int occ_combine = 1;          // NEXT-4 combine kernel
   bool ext = false;           // N > p: extended code of Eq. (qext)
   std::mutex mu;              // serialises the shared single-stripe plans' program buffer
   zp::ExtProg* d_prog = nullptr;
@@ -279,12 +280,15 @@ raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, 
   if (pl->fe && pl->ext && !pl->fe->kernel_ext[0]) pl->fe = nullptr;  // no fast extended kernels: generic
   if (pl->fe) {
     DeviceGuard g(device);
-    for (int m = 0; m < 4; m++) {
+    for (int m = 0; m < 5; m++) {
       const void* k = pl->ext ? pl->fe->kernel_ext[m] : pl->fe->kernel[m];
       const size_t sm = pl->ext ? pl->fe->smem_ext[m] : pl->fe->smem_bytes[m];
       raid6c_status st = kernel_occupancy(device, k, pl->fe->threads + 32, sm, &pl->occ[m]);
       if (st != RAID6C_OK) return st;
     }
+    raid6c_status st = kernel_occupancy(device, pl->ext ? pl->fe->combine_ext : pl->fe->combine,
+                                        pl->fe->combine_threads, pl->fe->combine_smem, &pl->occ_combine);
+    if (st != RAID6C_OK) return st;
   }
   return RAID6C_OK;
 }
@@ -319,6 +323,11 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
     if (mode == zp::KMODE_UPDATE) {
       aligned &= (reinterpret_cast<uintptr_t>(a.nbase) & 15u) == 0;
       if (a.num_stripes > 1) aligned &= a.new_stride % 16 == 0;
+    }
+    if (mode == zp::KMODE_PARTIAL) {  // TMA stores into the owners' slots
+      for (int g = 0; g < a.nranges; g++)
+        aligned &= ((reinterpret_cast<uintptr_t>(a.part_p[g]) | reinterpret_cast<uintptr_t>(a.part_q[g])) & 15u) == 0;
+      if (a.num_stripes > 1) aligned &= a.part_stride % 16 == 0;
     }
     const uint64_t TB = static_cast<uint64_t>(fe->tile_bytes), CB = static_cast<uint64_t>(fe->chunk_bytes);
     a.body_tiles = aligned ? pl->bytes / TB : 0;
@@ -367,6 +376,46 @@ raid6c_status strided_args(raid6c_plan pl, const uint8_t* data, size_t strip_str
   a.ei = pl->N;
   a.ej = pl->N + 1;
   return RAID6C_OK;
+}
+
+// NEXT-4 combine + solve over bytes [a.range_lo, a.range_hi) of every stripe.
+raid6c_status launch_combine(raid6c_plan pl, zp::ZpArgs& a, cudaStream_t st) {
+  if (a.num_stripes == 0 || a.range_hi <= a.range_lo) return RAID6C_OK;
+  a.N = pl->N;
+  a.bytes = pl->bytes;
+  a.pbytes = pl->pbytes;
+  cudaError_t err;
+  if (pl->fe) {
+    const zp::FastEntry* fe = pl->fe;
+    const uint64_t units = (a.range_hi - a.range_lo + fe->chunk_bytes - 1) / fe->chunk_bytes;
+    const uint64_t need = (units * static_cast<uint64_t>(a.num_stripes) + fe->combine_threads - 1) / fe->combine_threads;
+    uint64_t grid = std::min<uint64_t>(static_cast<uint64_t>(pl->num_sms) * pl->occ_combine, need);
+    if (grid == 0) grid = 1;
+    void* args[] = {&a};
+    err = cudaLaunchKernel(pl->ext ? fe->combine_ext : fe->combine, dim3(static_cast<unsigned>(grid)),
+                           dim3(fe->combine_threads), args, fe->combine_smem, st);
+  } else {
+    err = zp::generic_launch(a, pl->p, zp::KMODE_COMBINE, st, pl->num_sms);
+  }
+  if (err != cudaSuccess) {
+    pl->sticky = RAID6C_E_CUDA;
+    return cuda_fail(err);
+  }
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return RAID6C_OK;
+}
+
+// Word-range granule of p's kernels: a TMA tile (fast path) or lcm(byte group, 16) (generic).
+uint64_t range_granule_p(int p) {
+  if (const zp::FastEntry* fe = zp::fast_entry(p)) return static_cast<uint64_t>(fe->tile_bytes);
+  const int n = p - 1;
+  const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);
+  const uint64_t gb = static_cast<uint64_t>(g) * n / 8;
+  return gb * 16 / std::gcd<uint64_t>(gb, 16);
+}
+uint64_t range_granule(raid6c_plan pl) {
+  if (pl->fe) return static_cast<uint64_t>(pl->fe->tile_bytes);
+  return range_granule_p(pl->p);
 }
 
 // Upload host erasure pairs (validated, canonical) into the plan's device buffer.
@@ -442,6 +491,52 @@ raid6c_status upload_programs(raid6c_plan pl, const std::vector<int2>& pairs, cu
   }
   // pageable source: the copy is staged before this call returns, so `h` may be freed
   ZP_CUDA(cudaMemcpyAsync(pl->d_prog, h.data(), S * sizeof(zp::ExtProg), cudaMemcpyHostToDevice, st));
+  return RAID6C_OK;
+}
+
+// Erasure pairs of a batched call into the launch args (host array: validated and uploaded or
+// passed by value; device array: used in place).  with_programs: the extended code's
+// per-stripe multipliers (ExtProg) for the DP / DD solves are built and uploaded too.
+raid6c_status set_erasures(raid6c_plan plan, zp::ZpArgs& a, const raid6c_erasure* erasures, int num_erasures,
+                           int erasures_on_device, int num_stripes, bool with_programs) {
+  raid6c_status st = RAID6C_OK;
+  if (num_erasures != 1 && num_erasures != num_stripes) return RAID6C_E_SIZE;
+  if (plan->ext && with_programs) {  // extended code: per-stripe multipliers are built on the host from the pairs
+    std::vector<raid6c_erasure> hp(num_erasures);
+    if (erasures_on_device) {
+      ZP_CUDA(cudaMemcpy(hp.data(), erasures, num_erasures * sizeof(raid6c_erasure), cudaMemcpyDeviceToHost));
+    } else {
+      std::copy(erasures, erasures + num_erasures, hp.begin());
+    }
+    std::vector<int2> pairs(num_erasures);
+    for (int s2 = 0; s2 < num_erasures; s2++) {
+      st = check_erasure(plan->N, hp[s2].lost_i, hp[s2].lost_j);
+      if (st != RAID6C_OK) return st;
+      pairs[s2] = make_int2(std::min(hp[s2].lost_i, hp[s2].lost_j), std::max(hp[s2].lost_i, hp[s2].lost_j));
+    }
+    st = upload_programs(plan, pairs, plan->stream);
+    if (st != RAID6C_OK) return st;
+    a.prog = plan->d_prog;
+    a.prog_stride = num_erasures == 1 ? 0 : 1;
+  }
+  if (erasures_on_device) {
+    a.er = reinterpret_cast<const int2*>(erasures);
+    a.er_stride = num_erasures == 1 ? 0 : 1;
+  } else if (num_erasures == 1) {
+    st = check_erasure(plan->N, erasures[0].lost_i, erasures[0].lost_j);
+    if (st != RAID6C_OK) return st;
+    a.ei = std::min(erasures[0].lost_i, erasures[0].lost_j);
+    a.ej = std::max(erasures[0].lost_i, erasures[0].lost_j);
+  } else {
+    for (int s = 0; s < num_erasures; s++) {
+      st = check_erasure(plan->N, erasures[s].lost_i, erasures[s].lost_j);
+      if (st != RAID6C_OK) return st;
+    }
+    st = upload_erasures(plan, erasures, num_erasures, plan->stream);
+    if (st != RAID6C_OK) return st;
+    a.er = plan->d_er;
+    a.er_stride = 1;
+  }
   return RAID6C_OK;
 }
 
@@ -816,44 +911,9 @@ raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t* data, size_t str
   raid6c_status st = strided_args(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, a);
   if (st != RAID6C_OK) return st;
   if (!erasures) return RAID6C_E_NULL;
-  if (num_erasures != 1 && num_erasures != num_stripes) return RAID6C_E_SIZE;
   DeviceGuard g(plan->device);
-  if (plan->ext) {  // extended code: per-stripe multipliers are built on the host from the pairs
-    std::vector<raid6c_erasure> hp(num_erasures);
-    if (erasures_on_device) {
-      ZP_CUDA(cudaMemcpy(hp.data(), erasures, num_erasures * sizeof(raid6c_erasure), cudaMemcpyDeviceToHost));
-    } else {
-      std::copy(erasures, erasures + num_erasures, hp.begin());
-    }
-    std::vector<int2> pairs(num_erasures);
-    for (int s2 = 0; s2 < num_erasures; s2++) {
-      st = check_erasure(plan->N, hp[s2].lost_i, hp[s2].lost_j);
-      if (st != RAID6C_OK) return st;
-      pairs[s2] = make_int2(std::min(hp[s2].lost_i, hp[s2].lost_j), std::max(hp[s2].lost_i, hp[s2].lost_j));
-    }
-    st = upload_programs(plan, pairs, plan->stream);
-    if (st != RAID6C_OK) return st;
-    a.prog = plan->d_prog;
-    a.prog_stride = num_erasures == 1 ? 0 : 1;
-  }
-  if (erasures_on_device) {
-    a.er = reinterpret_cast<const int2*>(erasures);
-    a.er_stride = num_erasures == 1 ? 0 : 1;
-  } else if (num_erasures == 1) {
-    st = check_erasure(plan->N, erasures[0].lost_i, erasures[0].lost_j);
-    if (st != RAID6C_OK) return st;
-    a.ei = std::min(erasures[0].lost_i, erasures[0].lost_j);
-    a.ej = std::max(erasures[0].lost_i, erasures[0].lost_j);
-  } else {
-    for (int s = 0; s < num_erasures; s++) {
-      st = check_erasure(plan->N, erasures[s].lost_i, erasures[s].lost_j);
-      if (st != RAID6C_OK) return st;
-    }
-    st = upload_erasures(plan, erasures, num_erasures, plan->stream);
-    if (st != RAID6C_OK) return st;
-    a.er = plan->d_er;
-    a.er_stride = 1;
-  }
+  st = set_erasures(plan, a, erasures, num_erasures, erasures_on_device, num_stripes, true);
+  if (st != RAID6C_OK) return st;
   return launch(plan, a, zp::KMODE_RECOVER, plan->stream);
 }
 
@@ -903,6 +963,145 @@ raid6c_status raid6c_update_strided(raid6c_plan plan, uint8_t* data, size_t stri
     a.upd_stride = 2;
   }
   return launch(plan, a, zp::KMODE_UPDATE, plan->stream);
+}
+
+// ---------------------------------------------------------------- NEXT-4: cross-GPU stripe layout
+size_t raid6c_xgpu_range_bytes(int p, size_t bytes, int num_ranks) {
+  if (!is_valid_p(p) || bytes == 0 || num_ranks < 1 || num_ranks > RAID6C_MAX_RANKS) return 0;
+  const uint64_t gr = range_granule_p(p);
+  const uint64_t units = (parity_bytes(p, bytes) + gr - 1) / gr;
+  return static_cast<size_t>(((units + num_ranks - 1) / num_ranks) * gr);
+}
+
+// Strip table of a cross-GPU call: N+2 global-index pointers, strides.
+static raid6c_status xgpu_args(raid6c_plan plan, const uint8_t* const* strips, size_t data_stride, size_t parity_stride,
+                               int num_stripes, int k_lo, int k_hi, zp::ZpArgs& a) {
+  if (!plan || !strips) return RAID6C_E_NULL;
+  if (num_stripes < 0) return RAID6C_E_SIZE;
+  if (k_lo < 0 || k_hi > plan->N + 2 || k_lo > k_hi) return RAID6C_E_INVALID_INDEX;
+  for (int k = k_lo; k < k_hi; k++)
+    if (!strips[k]) return RAID6C_E_NULL;
+  if (num_stripes > 1 && (data_stride < plan->bytes || parity_stride < plan->pbytes)) return RAID6C_E_SIZE;
+  std::memset(&a, 0, sizeof(a));
+  for (int k = 0; k < plan->N + 2; k++) a.base[k] = strips[k];
+  a.data_stride = data_stride;
+  a.parity_stride = parity_stride;
+  a.num_stripes = num_stripes;
+  a.ei = plan->N;  // encode = the PQ pair
+  a.ej = plan->N + 1;
+  a.k_lo = k_lo;
+  a.k_hi = k_hi;
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_partial_strided(raid6c_plan plan, const uint8_t* const* strips, size_t data_stride,
+                                     size_t parity_stride, int num_stripes, const raid6c_erasure* erasures,
+                                     int num_erasures, int erasures_on_device, int k_lo, int k_hi, int num_ranges,
+                                     uint8_t* const* part_p, uint8_t* const* part_q, size_t part_stride,
+                                     size_t range_bytes) {
+  zp::ZpArgs a;
+  raid6c_status st = xgpu_args(plan, strips, data_stride, parity_stride, num_stripes, k_lo, k_hi, a);
+  if (st != RAID6C_OK) return st;
+  if (num_ranges < 1 || num_ranges > RAID6C_MAX_RANKS) return RAID6C_E_SIZE;
+  if (!part_p || !part_q) return RAID6C_E_NULL;
+  const uint64_t gr = range_granule(plan);
+  if (range_bytes == 0 || range_bytes % gr != 0 || static_cast<uint64_t>(range_bytes) * num_ranges < plan->pbytes)
+    return RAID6C_E_SIZE;
+  if (num_stripes > 1 && part_stride < range_bytes) return RAID6C_E_SIZE;
+  const int used = static_cast<int>((plan->pbytes + range_bytes - 1) / range_bytes);  // ranges holding bytes
+  for (int g = 0; g < used; g++)
+    if (!part_p[g] || !part_q[g]) return RAID6C_E_NULL;
+  for (int g = 0; g < num_ranges; g++) {
+    a.part_p[g] = part_p[g];
+    a.part_q[g] = part_q[g];
+  }
+  a.nranges = used;
+  a.range_bytes = range_bytes;
+  a.part_stride = part_stride;
+  DeviceGuard g(plan->device);
+  if (erasures) {
+    st = set_erasures(plan, a, erasures, num_erasures, erasures_on_device, num_stripes, false);
+    if (st != RAID6C_OK) return st;
+  }
+  return launch(plan, a, zp::KMODE_PARTIAL, plan->stream);
+}
+
+raid6c_status raid6c_combine_strided(raid6c_plan plan, uint8_t* const* strips, size_t data_stride,
+                                     size_t parity_stride, int num_stripes, const raid6c_erasure* erasures,
+                                     int num_erasures, int erasures_on_device, int num_sources,
+                                     const uint8_t* const* src_p, const uint8_t* const* src_q, size_t part_stride,
+                                     size_t range_lo, size_t range_hi) {
+  zp::ZpArgs a;
+  raid6c_status st = xgpu_args(plan, strips, data_stride, parity_stride, num_stripes, 0, 0, a);
+  if (st != RAID6C_OK) return st;
+  if (num_sources < 1 || num_sources > RAID6C_MAX_RANKS) return RAID6C_E_SIZE;
+  if (!src_p || !src_q) return RAID6C_E_NULL;
+  for (int r = 0; r < num_sources; r++) {
+    if (!src_p[r] || !src_q[r]) return RAID6C_E_NULL;
+    a.src_p[r] = src_p[r];
+    a.src_q[r] = src_q[r];
+  }
+  const uint64_t gr = range_granule(plan);
+  if (range_lo % gr != 0 || range_hi < range_lo || range_hi > plan->pbytes) return RAID6C_E_SIZE;
+  if (num_stripes > 1 && part_stride < range_hi - range_lo) return RAID6C_E_SIZE;
+  a.nsrc = num_sources;
+  a.range_lo = range_lo;
+  a.range_hi = range_hi;
+  a.part_stride = part_stride;
+  DeviceGuard g(plan->device);
+  if (erasures) {
+    st = set_erasures(plan, a, erasures, num_erasures, erasures_on_device, num_stripes, true);
+    if (st != RAID6C_OK) return st;
+  }
+  // output strips of every stripe must be present: check against the (host-known) pairs
+  if (!erasures || !erasures_on_device) {
+    for (int s = 0; s < (erasures ? num_erasures : 1); s++) {
+      const int x = erasures ? std::min(erasures[s].lost_i, erasures[s].lost_j) : plan->N;
+      const int y = erasures ? std::max(erasures[s].lost_i, erasures[s].lost_j) : plan->N + 1;
+      if (!strips[x] || !strips[y]) return RAID6C_E_NULL;
+    }
+  }
+  return launch_combine(plan, a, plan->stream);
+}
+
+raid6c_status raid6c_dev_alloc(size_t bytes, int device, void** dev_ptr) {
+  if (!dev_ptr) return RAID6C_E_NULL;
+  *dev_ptr = nullptr;
+  if (bytes == 0) return RAID6C_E_SIZE;
+  DeviceGuard g(device);
+  ZP_CUDA(cudaMalloc(dev_ptr, bytes));
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_dev_free(void* dev_ptr) {
+  if (!dev_ptr) return RAID6C_E_NULL;
+  ZP_CUDA(cudaFree(dev_ptr));
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_ipc_export(const void* dev_ptr, uint8_t handle[64]) {
+  if (!dev_ptr || !handle) return RAID6C_E_NULL;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
+  cudaIpcMemHandle_t h;
+  ZP_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memcpy(handle, &h, 64);
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_ipc_open(const uint8_t handle[64], int device, void** dev_ptr) {
+  if (!handle || !dev_ptr) return RAID6C_E_NULL;
+  *dev_ptr = nullptr;
+  DeviceGuard g(device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  ZP_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return RAID6C_E_NULL;
+  ZP_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return RAID6C_OK;
 }
 
 // ---------------------------------------------------------------- NEXT-3: GF(256) RS baseline

@@ -47,6 +47,21 @@ struct ZpArgs {
   // NEXT-2: multiplier programs for the extended code (prog[s * prog_stride]); N > p only.
   const ExtProg* prog;
   int prog_stride;
+  // NEXT-4 (cross-GPU stripe layout, include/raid6c.h).  partial: rows = the surviving strips
+  // with global index in [k_lo, k_hi); word range g of its two outputs goes to
+  // part_p[g] / part_q[g] + s*part_stride + (off - g*range_bytes).
+  int k_lo, k_hi;
+  int nranges;
+  uint64_t range_bytes;
+  uint64_t part_stride;
+  uint8_t* part_p[RAID6C_MAX_RANKS];
+  uint8_t* part_q[RAID6C_MAX_RANKS];
+  // combine: bytes [range_lo, range_hi) of every stripe from nsrc partial slots
+  // (src_p[r] / src_q[r] + s*part_stride), then the class solve; outputs to base[k].
+  int nsrc;
+  uint64_t range_lo, range_hi;
+  const uint8_t* src_p[RAID6C_MAX_RANKS];
+  const uint8_t* src_q[RAID6C_MAX_RANKS];
 };
 
 // Kernel-geometry record for one compiled prime (fast path) -- filled by each
@@ -56,16 +71,21 @@ struct FastEntry {
   int chunk_bytes;  // bytes per thread-chunk (whole periods of lcm(n,32) bits)
   int tile_bytes;   // TMA row bytes = consumer threads * chunk_bytes
   int threads;      // consumer threads (+32 producer threads per CTA)
-  const void* kernel[4];  // __global__ void(ZpArgs) per mode: encode, recover, scrub, update
-  size_t smem_bytes[4];
-  const void* kernel_ext[4];  // extended-code (N > p) kernels, nullptr if p fails Theorem 25.3
-  size_t smem_ext[4];
+  const void* kernel[5];  // __global__ void(ZpArgs) per mode: encode, recover, scrub, update, partial
+  size_t smem_bytes[5];
+  const void* kernel_ext[5];  // extended-code (N > p) kernels, nullptr if p fails Theorem 25.3
+  size_t smem_ext[5];
+  const void* combine;      // NEXT-4 combine + solve kernel (basic code)
+  const void* combine_ext;  // (extended code; nullptr if p fails Theorem 25.3)
+  size_t combine_smem;
+  int combine_threads;
 };
 
 const FastEntry* fast_entry(int p);  // nullptr if p has no fast path
 
 // Generic (runtime-p) kernels, any odd prime <= 257.
-enum : int { KMODE_ENCODE = 0, KMODE_RECOVER = 1, KMODE_SCRUB = 2, KMODE_UPDATE = 3 };
+enum : int { KMODE_ENCODE = 0, KMODE_RECOVER = 1, KMODE_SCRUB = 2, KMODE_UPDATE = 3, KMODE_PARTIAL = 4,
+             KMODE_COMBINE = 5 };
 cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, int num_sms);
 
 }  // namespace zp

@@ -278,8 +278,13 @@ __device__ __forceinline__ void reduce(const Acc<G>& acc, uint32_t (&V)[G::C]) {
 // ------------------------------------------------------------------ stripe bookkeeping
 enum : int { CLS_PQ = 0, CLS_DQ = 1, CLS_DP = 2, CLS_DD = 3, CLS_SCRUB = 4, CLS_UPDATE = 5 };
 // Kernel modes (compile-time): the method's two operations and the NEXT-1 pair around them.
-enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3 };
-constexpr int K_NEW = -1;  // row index of the update's new-data buffer
+// MODE_PARTIAL (NEXT-4): the fold of a recovery (or encode) restricted to the strips held by one
+// rank, stored unsolved as partial syndromes (dP_r, dQ_r) into the word-range owners' slots.
+enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3, MODE_PARTIAL = 4 };
+constexpr int NUM_MODES = 5;
+constexpr int K_NEW = -1;     // row index of the update's new-data buffer
+constexpr int K_PART_P = -2;  // partial-mode outputs (slots of the word-range owners)
+constexpr int K_PART_Q = -3;
 
 struct ItemDesc {
   int x, y;   // canonical lost pair, x < y (update: x = the rewritten strip)
@@ -303,7 +308,7 @@ __device__ __forceinline__ ItemDesc item_desc(const ZpArgs& a, int s) {
     return d;
   } else {
     int i = a.N, j = a.N + 1;
-    if constexpr (MODE == MODE_RECOVER) {
+    if constexpr (MODE == MODE_RECOVER || MODE == MODE_PARTIAL) {
       if (a.er) {
         const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
         i = e.x; j = e.y;
@@ -323,8 +328,11 @@ __device__ __forceinline__ ItemDesc item_desc(const ZpArgs& a, int s) {
 }
 
 template <int MODE>
-__device__ __forceinline__ int num_rows(const ZpArgs& a) {
+__device__ __forceinline__ int num_rows(const ZpArgs& a, const ItemDesc& d) {
   if constexpr (MODE == MODE_SCRUB) return a.N + 2;     // every strip of the stripe
+  // the surviving strips held by this rank: global indices [k_lo, k_hi) minus the lost pair
+  else if constexpr (MODE == MODE_PARTIAL)
+    return a.k_hi - a.k_lo - (d.x >= a.k_lo && d.x < a.k_hi) - (d.y >= a.k_lo && d.y < a.k_hi);
   // old d_k, new d_k, P, Q: the count (4) comes from the launch args so that the compiler keeps
   // the row loop rolled (a compile-time 4 unrolls it and spills the accumulators)
   else if constexpr (MODE == MODE_UPDATE) return a.upd_rows;
@@ -340,9 +348,18 @@ __device__ __forceinline__ int source_strip(int r, const ItemDesc& d) {
 }
 
 // Strip index read by row r (K_NEW = the update's new-data buffer).
+// r-th surviving strip at or above k_lo (partial mode), skipping the lost pair (x < y).
+__device__ __forceinline__ int source_strip_from(int r, int k_lo, const ItemDesc& d) {
+  int k = k_lo + r;
+  if (d.x >= k_lo && k >= d.x) k++;
+  if (d.y >= k_lo && k >= d.y) k++;
+  return k;
+}
+
 template <int MODE>
 __device__ __forceinline__ int row_strip(const ZpArgs& a, int r, const ItemDesc& d) {
   if constexpr (MODE == MODE_SCRUB) return r;
+  else if constexpr (MODE == MODE_PARTIAL) return source_strip_from(r, a.k_lo, d);
   else if constexpr (MODE == MODE_UPDATE) return r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
   else return source_strip(r, d);
 }
@@ -354,7 +371,19 @@ __device__ __forceinline__ const uint8_t* row_ptr(const ZpArgs& a, int k, int s)
   return k == K_NEW ? a.nbase + static_cast<uint64_t>(s) * a.new_stride
                     : a.base[k] + static_cast<uint64_t>(s) * strip_stride(a, k);
 }
-__device__ __forceinline__ uint64_t row_len(const ZpArgs& a, int k) { return k < a.N ? a.bytes : a.pbytes; }
+__device__ __forceinline__ uint64_t row_len(const ZpArgs& a, int k) {
+  return (k >= 0 && k < a.N) ? a.bytes : a.pbytes;
+}
+// Output address of byte `off` of output strip k of stripe s (partial outputs: the slot of the
+// owner of the word range containing `off`; ranges are whole tiles, so a tile has one owner).
+__device__ __forceinline__ uint8_t* out_ptr(const ZpArgs& a, int k, int s, uint64_t off) {
+  if (k == K_PART_P || k == K_PART_Q) {
+    const int g = static_cast<int>(off / a.range_bytes);
+    uint8_t* base = (k == K_PART_P) ? a.part_p[g] : a.part_q[g];
+    return base + static_cast<uint64_t>(s) * a.part_stride + (off - static_cast<uint64_t>(g) * a.range_bytes);
+  }
+  return const_cast<uint8_t*>(row_ptr(a, k, s)) + off;
+}
 
 // acc += g_k * S for the extended code's coefficient of data strip k (Eq. (qext)):
 // x^k for k < p, 1 + x^{k-p+1} for k >= p.
@@ -576,6 +605,22 @@ __host__ __device__ constexpr int num_outputs() {
   return MODE == MODE_SCRUB ? 0 : (MODE == MODE_UPDATE ? 3 : 2);
 }
 
+// Mask table MX(a), ML(a) per lane phase (positions are word-relative, chunk starts at a word).
+template <class G>
+__device__ __forceinline__ void build_mtab(uint2* mtab) {
+  for (int e = threadIdx.x; e < G::MTAB; e += blockDim.x) {
+    const int am = e / G::LAMBDA, phi = e % G::LAMBDA;
+    uint32_t mx = 0, ml = 0;
+    int pos = (32 * phi) % G::n;
+    for (int b = 0; b < 32; b++) {
+      if (pos >= am || pos == 0) mx |= 1u << b;
+      if (pos + 2 <= am) ml |= 1u << b;
+      if (++pos == G::n) pos = 0;
+    }
+    mtab[e] = make_uint2(mx, ml);
+  }
+}
+
 // Shared-memory layout per (p, mode): STAGES TMA rows, NOUT output rows, mask table, barriers.
 template <int P, int MODE>
 struct Layout {
@@ -611,6 +656,12 @@ __device__ __forceinline__ void epilogue(const ZpArgs& a, const ItemDesc& d, int
     for (int l = 0; l < C; l++) o0[l] = Pa[l];
     reduce<G>(acc, o1);
     k0 = a.N; k1 = a.N + 1; k2 = d.x;
+  } else if constexpr (MODE == MODE_PARTIAL) {
+    // unsolved partial syndromes; pi is a homomorphism, so reduced partials add up (NEXT-4)
+#pragma unroll
+    for (int l = 0; l < C; l++) o0[l] = Pa[l];
+    reduce<G>(acc, o1);
+    k0 = K_PART_P; k1 = K_PART_Q;
   } else if constexpr (EXT) {
     finish_ext<G>(a, d, s, Pa, acc, mtab, o0, o1, k0, k1);
   } else {
@@ -633,18 +684,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
 
-  // Mask table MX(a), ML(a) per lane phase (positions are word-relative, chunk starts at a word).
-  for (int e = tid; e < G::MTAB; e += blockDim.x) {
-    const int am = e / G::LAMBDA, phi = e % G::LAMBDA;
-    uint32_t mx = 0, ml = 0;
-    int pos = (32 * phi) % G::n;
-    for (int b = 0; b < 32; b++) {
-      if (pos >= am || pos == 0) mx |= 1u << b;
-      if (pos + 2 <= am) ml |= 1u << b;
-      if (++pos == G::n) pos = 0;
-    }
-    mtab[e] = make_uint2(mx, ml);
-  }
+  build_mtab<G>(mtab);
   if (tid == 0) {
     for (int s = 0; s < ST; s++) {
       mbar_init(&full[s], 1);
@@ -656,7 +696,6 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
 
   const uint64_t tiles = a.body_tiles;
   const uint64_t body_items = tiles * static_cast<uint64_t>(a.num_stripes);
-  const int R = num_rows<MODE>(a);
 
   if (warp == NT / 32) {
     // ------------------------------------------------ producer: one lane issues all TMA rows
@@ -666,6 +705,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
         const int s = static_cast<int>(it / tiles);
         const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
         const ItemDesc d = item_desc<MODE, EXT>(a, s);
+        const int R = num_rows<MODE>(a, d);
         for (int r = 0; r < R; r++) {
           const uint8_t* g = row_ptr(a, row_strip<MODE>(a, r, d), s) + t * TB;
           mbar_wait(&empty[stage], ph ^ 1u);
@@ -684,6 +724,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
     const int s = static_cast<int>(it / tiles);
     const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
     const ItemDesc d = item_desc<MODE, EXT>(a, s);
+    const int R = num_rows<MODE>(a, d);
     uint32_t Pa[C];
     uint32_t NEW[C];  // unused in the body path (update stages the new row in SMEM)
     Acc<G> acc;
@@ -726,9 +767,9 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
       fence_proxy_async_smem();
       named_bar_sync(1, NT);
       if (tid == 0) {
-        tma_store_row(const_cast<uint8_t*>(row_ptr(a, k0, s)) + t * TB, outb, TB);
-        tma_store_row(const_cast<uint8_t*>(row_ptr(a, k1, s)) + t * TB, outb + TB, TB);
-        if constexpr (NOUT == 3) tma_store_row(const_cast<uint8_t*>(row_ptr(a, k2, s)) + t * TB, outb + 2 * TB, TB);
+        tma_store_row(out_ptr(a, k0, s, t * TB), outb, TB);
+        tma_store_row(out_ptr(a, k1, s, t * TB), outb + TB, TB);
+        if constexpr (NOUT == 3) tma_store_row(out_ptr(a, k2, s, t * TB), outb + 2 * TB, TB);
         bulk_commit();
       }
     }
@@ -743,6 +784,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
     const int s = static_cast<int>(u / tups);
     const uint64_t off = body_end + (u - static_cast<uint64_t>(s) * tups) * CB;
     const ItemDesc d = item_desc<MODE, EXT>(a, s);
+    const int R = num_rows<MODE>(a, d);
     uint32_t Pa[C];
     uint32_t NEW[C];  // update mode only (dead otherwise)
     Acc<G> acc;
@@ -768,12 +810,59 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
       epilogue<MODE, G, false, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
     } else {
       epilogue<MODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
-      st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k0, s)) + off, off, row_len(a, k0), o0);
-      st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k1, s)) + off, off, row_len(a, k1), o1);
+      st_chunk_global<C>(out_ptr(a, k0, s, off), off, row_len(a, k0), o0);
+      st_chunk_global<C>(out_ptr(a, k1, s, off), off, row_len(a, k1), o1);
     }
   }
   if constexpr (NOUT > 0)
     if (tid == 0) bulk_wait0();
+}
+
+// ------------------------------------------------------------------ NEXT-4 combine + solve
+// Owner of word range [range_lo, range_hi): sum the nsrc partial syndromes of the range (its own
+// slots, or peer pointers over NVLink) and run the class epilogue of the recovery (encode = PQ)
+// in the same pass, storing the rebuilt strips straight to their owners (a.base[k], possibly
+// peer memory).  One thread per chunk; the solve is identical to zp_kernel's epilogue.
+constexpr int COMBINE_THREADS = 256;
+
+template <int P, bool EXT = false>
+__global__ void __launch_bounds__(COMBINE_THREADS) zp_combine_kernel(const __grid_constant__ ZpArgs a) {
+  using G = Geo<P>;
+  constexpr int C = G::C, CB = G::CB;
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint2* mtab = reinterpret_cast<uint2*>(smem);
+  build_mtab<G>(mtab);
+  __syncthreads();
+  const uint64_t units = (a.range_hi - a.range_lo + CB - 1) / CB;
+  const uint64_t total = units * static_cast<uint64_t>(a.num_stripes);
+  for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
+       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(u / units);
+    const uint64_t roff = (u - static_cast<uint64_t>(s) * units) * CB;  // offset inside the range
+    const uint64_t off = a.range_lo + roff;                               // offset inside the strip
+    const ItemDesc d = item_desc<MODE_RECOVER, EXT>(a, s);
+    uint32_t Pa[C], NEW[C];
+    Acc<G> acc;
+    acc.zero();
+#pragma unroll
+    for (int l = 0; l < C; l++) Pa[l] = 0;
+    const uint64_t so = static_cast<uint64_t>(s) * a.part_stride + roff;
+#pragma unroll 1
+    for (int r = 0; r < a.nsrc; r++) {
+      uint32_t L[C];
+      ld_chunk_global<C>(a.src_p[r] + so, off, a.pbytes, L);
+#pragma unroll
+      for (int l = 0; l < C; l++) Pa[l] ^= L[l];
+      ld_chunk_global<C>(a.src_q[r] + so, off, a.pbytes, L);
+#pragma unroll
+      for (int l = 0; l < C; l++) acc.ay[l] ^= L[l];  // reduced words: rotation by 0
+    }
+    uint32_t o0[C], o1[C];
+    int k0 = 0, k1 = 0, k2 = 0;
+    epilogue<MODE_RECOVER, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+    st_chunk_global<C>(out_ptr(a, k0, s, off), off, row_len(a, k0), o0);
+    st_chunk_global<C>(out_ptr(a, k1, s, off), off, row_len(a, k1), o1);
+  }
 }
 
 template <int P, bool WITH_EXT>
@@ -788,6 +877,11 @@ FastEntry make_entry() {
   e.kernel[MODE_RECOVER] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_RECOVER>);
   e.kernel[MODE_SCRUB] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_SCRUB>);
   e.kernel[MODE_UPDATE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_UPDATE>);
+  e.kernel[MODE_PARTIAL] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_PARTIAL>);
+  e.smem_bytes[MODE_PARTIAL] = Layout<P, MODE_PARTIAL>::SMEM;
+  e.combine = reinterpret_cast<const void*>(&zp_combine_kernel<P, false>);
+  e.combine_smem = static_cast<size_t>(G::MTAB) * 8;
+  e.combine_threads = COMBINE_THREADS;
   e.smem_bytes[MODE_ENCODE] = Layout<P, MODE_ENCODE>::SMEM;
   e.smem_bytes[MODE_RECOVER] = Layout<P, MODE_RECOVER>::SMEM;
   e.smem_bytes[MODE_SCRUB] = Layout<P, MODE_SCRUB>::SMEM;
@@ -797,6 +891,9 @@ FastEntry make_entry() {
     e.kernel_ext[MODE_RECOVER] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_RECOVER, true>);
     e.kernel_ext[MODE_SCRUB] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_SCRUB, true>);
     e.kernel_ext[MODE_UPDATE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_UPDATE, true>);
+    e.kernel_ext[MODE_PARTIAL] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_PARTIAL, true>);
+    e.smem_ext[MODE_PARTIAL] = Layout<P, MODE_PARTIAL>::SMEM;
+    e.combine_ext = reinterpret_cast<const void*>(&zp_combine_kernel<P, true>);
     e.smem_ext[MODE_ENCODE] = Layout<P, MODE_ENCODE>::SMEM;
     e.smem_ext[MODE_RECOVER] = Layout<P, MODE_RECOVER>::SMEM;
     e.smem_ext[MODE_SCRUB] = Layout<P, MODE_SCRUB>::SMEM;
@@ -815,6 +912,8 @@ FastEntry make_entry() {
   template __global__ void zp_kernel<PP, MODE_RECOVER>(const __grid_constant__ ZpArgs);       \
   template __global__ void zp_kernel<PP, MODE_SCRUB>(const __grid_constant__ ZpArgs);         \
   template __global__ void zp_kernel<PP, MODE_UPDATE>(const __grid_constant__ ZpArgs);        \
+  template __global__ void zp_kernel<PP, MODE_PARTIAL>(const __grid_constant__ ZpArgs);       \
+  template __global__ void zp_combine_kernel<PP, false>(const __grid_constant__ ZpArgs);      \
   const FastEntry* fast_entry_##PP() {                                                       \
     static const FastEntry e = make_entry<PP, WITH_EXT>();                                   \
     return &e;                                                                               \
@@ -827,5 +926,7 @@ FastEntry make_entry() {
   template __global__ void zp_kernel<PP, MODE_RECOVER, true>(const __grid_constant__ ZpArgs); \
   template __global__ void zp_kernel<PP, MODE_SCRUB, true>(const __grid_constant__ ZpArgs);   \
   template __global__ void zp_kernel<PP, MODE_UPDATE, true>(const __grid_constant__ ZpArgs);  \
+  template __global__ void zp_kernel<PP, MODE_PARTIAL, true>(const __grid_constant__ ZpArgs); \
+  template __global__ void zp_combine_kernel<PP, true>(const __grid_constant__ ZpArgs);       \
   }                                                                                          \
   ZP_INSTANTIATE_FAST_IMPL(PP, true)

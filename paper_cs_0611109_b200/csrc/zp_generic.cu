@@ -8,6 +8,7 @@
 //   * the class epilogues are the same as the fast path (Lemma 23.2 proof PAPER.md:380-401,
 //     Sec. 4.6), the DD inverse by the same doubling chain.
 // Correctness path: no TMA, no shared memory; used for primes outside the fast set.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -83,7 +84,7 @@ __device__ Desc desc_of(const ZpArgs& a, int s, int mode, int p) {
     return d;
   }
   int i = a.N, j = a.N + 1;
-  if (mode == KMODE_RECOVER) {
+  if (mode == KMODE_RECOVER || mode == KMODE_PARTIAL || mode == KMODE_COMBINE) {
     if (a.er) {
       const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
       i = e.x; j = e.y;
@@ -126,20 +127,42 @@ __device__ __forceinline__ uint64_t rlen(const ZpArgs& a, int k) { return k < a.
 
 constexpr int GROUP_MAX_BYTES = 128;  // g*n/8 <= n/2 <= 128
 
+// Group range of one launch: all groups of the strip, or (combine) the groups of bytes
+// [range_lo, range_hi) -- range_lo is a multiple of the group size (host-checked).
+__device__ __forceinline__ void group_span(const ZpArgs& a, int mode, int n, int g, int gbytes, uint64_t& g0,
+                                           uint64_t& g1) {
+  const uint64_t W = (8 * a.bytes + n - 1) / n;
+  const uint64_t groups = (W + g - 1) / g;
+  g0 = 0;
+  g1 = groups;
+  if (mode == KMODE_COMBINE) {
+    g0 = a.range_lo / gbytes;
+    const uint64_t e = (a.range_hi + gbytes - 1) / gbytes;
+    g1 = e < groups ? e : groups;
+    if (g1 < g0) g1 = g0;
+  }
+}
+
 __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int mode) {
   const int n = p - 1;
   const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);  // 8 / gcd(n, 8)
   const int gbytes = g * n / 8;
   const uint64_t W = (8 * a.bytes + n - 1) / n;
-  const uint64_t groups = (W + g - 1) / g;
+  uint64_t g0, g1;
+  group_span(a, mode, n, g, gbytes, g0, g1);
+  const uint64_t groups = g1 - g0;
   const uint64_t total = groups * static_cast<uint64_t>(a.num_stripes);
-  const int R = mode == KMODE_SCRUB ? a.N + 2 : (mode == KMODE_UPDATE ? a.upd_rows : a.N);
   for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
        u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int s = static_cast<int>(u / groups);
-    const uint64_t grp = u - static_cast<uint64_t>(s) * groups;
+    const uint64_t grp = g0 + (u - static_cast<uint64_t>(s) * groups);
     const Desc d = desc_of(a, s, mode, p);
     const bool ext = a.N > p;
+    // rows: partial = this rank's surviving strips [k_lo, k_hi); combine = nsrc partial slots
+    int R = mode == KMODE_SCRUB ? a.N + 2 : (mode == KMODE_UPDATE ? a.upd_rows : a.N);
+    if (mode == KMODE_PARTIAL)
+      R = a.k_hi - a.k_lo - (d.x >= a.k_lo && d.x < a.k_hi) - (d.y >= a.k_lo && d.y < a.k_hi);
+    if (mode == KMODE_COMBINE) R = a.nsrc;
     int kout[3] = {0, 0, 0};
     int nout = 2;
     if (d.cls == 0) { kout[0] = a.N; kout[1] = a.N + 1; }
@@ -159,13 +182,23 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
       wzero(acc);
       wzero(NEWW);
       for (int r = 0; r < R; r++) {
+        if (mode == KMODE_COMBINE) {  // partial slots hold reduced words of bytes [range_lo, ...)
+          const uint64_t so = static_cast<uint64_t>(s) * a.part_stride;
+          const uint64_t wl = w - (a.range_lo * 8) / n, ll = a.pbytes - a.range_lo;
+          load_word(a.src_p[r] + so, ll, wl, n, L);
+          wxor(Pa, L);
+          load_word(a.src_q[r] + so, ll, wl, n, L);
+          wxor(acc, L);
+          continue;
+        }
         int k;
         if (mode == KMODE_SCRUB) k = r;
         else if (mode == KMODE_UPDATE) k = r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
         else {
-          k = r;
-          if (k >= d.x) k++;
-          if (k >= d.y) k++;
+          k = mode == KMODE_PARTIAL ? a.k_lo + r : r;
+          const int lo = mode == KMODE_PARTIAL ? a.k_lo : 0;
+          if (d.x >= lo && k >= d.x) k++;
+          if (d.y >= lo && k >= d.y) k++;
         }
         load_word(rptr(a, k, s), rlen(a, k), w, n, L);
         if (k == K_NEW) {
@@ -184,7 +217,11 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
         }
       }
       const ExtProg* pr = ext ? a.prog + static_cast<int64_t>(s) * a.prog_stride : nullptr;
-      if (ext && (d.cls == 1 || d.cls == 2 || d.cls == 3)) {  // extended code (Lemma 23.2 with Eq. (qext))
+      if (mode == KMODE_PARTIAL) {  // unsolved partial syndromes (NEXT-4)
+        o[0] = Pa;
+        reduce(acc, p);
+        o[1] = acc;
+      } else if (ext && (d.cls == 1 || d.cls == 2 || d.cls == 3)) {  // extended code (Lemma 23.2 with Eq. (qext))
         if (d.cls == 1) {
           o[0] = Pa;
           add_coeff(acc, Pa, d.x, p);
@@ -267,10 +304,20 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
     }
     const uint64_t byte0 = grp * static_cast<uint64_t>(gbytes);
     for (int q = 0; q < nout; q++) {
-      uint8_t* gq = const_cast<uint8_t*>(rptr(a, kout[q], s));
-      const uint64_t len = rlen(a, kout[q]);
+      uint8_t* gq;  // address of byte byte0 of output q
+      uint64_t left;
+      if (mode == KMODE_PARTIAL) {  // slot of the owner of this word range
+        const int own = static_cast<int>(byte0 / a.range_bytes);
+        gq = (q == 0 ? a.part_p[own] : a.part_q[own]) + static_cast<uint64_t>(s) * a.part_stride +
+             (byte0 - static_cast<uint64_t>(own) * a.range_bytes);
+        left = a.pbytes > byte0 ? a.pbytes - byte0 : 0;
+      } else {
+        gq = const_cast<uint8_t*>(rptr(a, kout[q], s)) + byte0;
+        const uint64_t len = rlen(a, kout[q]);
+        left = len > byte0 ? len - byte0 : 0;
+      }
       for (int i = 0; i < gbytes; i++)
-        if (byte0 + i < len) gq[byte0 + i] = ob[q][i];
+        if (static_cast<uint64_t>(i) < left) gq[i] = ob[q][i];
     }
   }
 }
@@ -280,8 +327,15 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
 cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, int num_sms) {
   const int n = p - 1;
   const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);
+  const int gbytes = g * n / 8;
   const uint64_t W = (8 * a.bytes + n - 1) / n;
-  const uint64_t total = ((W + g - 1) / g) * static_cast<uint64_t>(a.num_stripes);
+  uint64_t g0 = 0, g1 = (W + g - 1) / g;
+  if (mode == KMODE_COMBINE) {
+    g0 = a.range_lo / gbytes;
+    g1 = std::min<uint64_t>(g1, (a.range_hi + gbytes - 1) / gbytes);
+    if (g1 < g0) g1 = g0;
+  }
+  const uint64_t total = (g1 - g0) * static_cast<uint64_t>(a.num_stripes);
   const int threads = 128;
   uint64_t blocks = (total + threads - 1) / threads;
   const uint64_t cap = static_cast<uint64_t>(num_sms) * 16;

@@ -54,6 +54,16 @@ _SIGS = [
     ("raid6c_update_strided", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _sz, _vp, _i, _i]),
     ("raid6c_rs_encode_strided", _i, [_i, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp]),
     ("raid6c_rs_recover_strided", _i, [_i, _sz, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _i, _i, _vp]),
+    ("raid6c_xgpu_range_bytes", _sz, [_i, _sz, _i]),
+    ("raid6c_partial_strided", _i, [_vp, ctypes.POINTER(_vp), _sz, _sz, _i, _vp, _i, _i, _i, _i, _i,
+                                    ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _sz]),
+    ("raid6c_combine_strided", _i, [_vp, ctypes.POINTER(_vp), _sz, _sz, _i, _vp, _i, _i, _i,
+                                    ctypes.POINTER(_vp), ctypes.POINTER(_vp), _sz, _sz, _sz]),
+    ("raid6c_dev_alloc", _i, [_sz, _i, ctypes.POINTER(_vp)]),
+    ("raid6c_dev_free", _i, [_vp]),
+    ("raid6c_ipc_export", _i, [_vp, ctypes.c_char_p]),
+    ("raid6c_ipc_open", _i, [ctypes.c_char_p, _i, ctypes.POINTER(_vp)]),
+    ("raid6c_ipc_close", _i, [_vp]),
     ("raid6c_encode_host", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i]),
     ("raid6c_recover_host", _i, [_vp, _vp, _sz, _sz, _vp, _vp, _sz, _i, _vp, _i]),
     ("raid6c_host_traffic", _i, [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
@@ -276,6 +286,79 @@ class Plan:
             self.recover_strided(data, ss, N * ss, parity, _ptr(parity) + ps, 2 * ps, S, erasures)
         else:
             self.recover_host(data, ss, N * ss, parity, _ptr(parity) + ps, 2 * ps, S, erasures)
+
+
+    # ------------------------------------------------ NEXT-4: cross-GPU stripe layout
+    def xgpu_range_bytes(self, num_ranks: int) -> int:
+        return xgpu_range_bytes(self.p, self.nbytes, num_ranks)
+
+    def _erasure_args(self, erasures):
+        """(pointer, count, on_device) for None (encode), host pairs, or an int32 CUDA tensor [S, 2]."""
+        if erasures is None:
+            return None, 0, 0, None
+        if hasattr(erasures, "is_cuda") and erasures.is_cuda:
+            return _ptr(erasures), int(erasures.shape[0]), 1, None
+        arr = _erasure_array(erasures)
+        return ctypes.cast(arr, _vp), len(arr), 0, arr
+
+    def partial_strided(self, strips, data_stride, parity_stride, num_stripes, erasures, k_lo, k_hi,
+                        part_p, part_q, part_stride, range_bytes):
+        """raid6c_partial_strided.  strips: N+2 device addresses by global index (None = not held);
+        part_p / part_q: one device address per word range (owner slots)."""
+        st = (_vp * (self.N + 2))(*[None if x is None else _ptr(x) for x in strips])
+        pp = (_vp * len(part_p))(*[_ptr(x) for x in part_p])
+        pq = (_vp * len(part_q))(*[_ptr(x) for x in part_q])
+        ep, en, eo, _keep = self._erasure_args(erasures)
+        _check(_lib.raid6c_partial_strided(self._h, st, data_stride, parity_stride, num_stripes, ep, en, eo, k_lo, k_hi,
+                                           len(part_p), pp, pq, part_stride, range_bytes), "raid6c_partial_strided")
+
+    def combine_strided(self, strips, data_stride, parity_stride, num_stripes, erasures, src_p, src_q, part_stride,
+                        range_lo, range_hi):
+        """raid6c_combine_strided.  strips: N+2 device addresses by global index (outputs written);
+        src_p / src_q: one device address per partial source."""
+        st = (_vp * (self.N + 2))(*[None if x is None else _ptr(x) for x in strips])
+        sp = (_vp * len(src_p))(*[_ptr(x) for x in src_p])
+        sq = (_vp * len(src_q))(*[_ptr(x) for x in src_q])
+        ep, en, eo, _keep = self._erasure_args(erasures)
+        _check(_lib.raid6c_combine_strided(self._h, st, data_stride, parity_stride, num_stripes, ep, en, eo, len(src_p),
+                                           sp, sq, part_stride, range_lo, range_hi), "raid6c_combine_strided")
+
+
+# ------------------------------------------------------------------ NEXT-4: cross-GPU layout helpers
+def xgpu_range_bytes(p: int, nbytes: int, num_ranks: int) -> int:
+    """raid6c_xgpu_range_bytes: word-range size for num_ranks owners (host only)."""
+    r = int(_lib.raid6c_xgpu_range_bytes(p, nbytes, num_ranks))
+    if r == 0:
+        raise Raid6Error(5, "raid6c_xgpu_range_bytes")
+    return r
+
+
+# ------------------------------------------------------------------ inter-process device memory (NEXT-4)
+def dev_alloc(nbytes: int, device: int) -> int:
+    h = _vp()
+    _check(_lib.raid6c_dev_alloc(nbytes, device, ctypes.byref(h)), "raid6c_dev_alloc")
+    return int(h.value)
+
+
+def dev_free(ptr: int) -> None:
+    _check(_lib.raid6c_dev_free(ptr), "raid6c_dev_free")
+
+
+def ipc_export(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(_lib.raid6c_ipc_export(ptr, buf), "raid6c_ipc_export")
+    return buf.raw
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    assert len(handle) == 64
+    h = _vp()
+    _check(_lib.raid6c_ipc_open(handle, device, ctypes.byref(h)), "raid6c_ipc_open")
+    return int(h.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(_lib.raid6c_ipc_close(ptr), "raid6c_ipc_close")
 
 
 def aligned_stride(nbytes: int, align: int = 256) -> int:
