@@ -482,6 +482,156 @@ def run_full(args):
         dist.destroy_process_group()
 
 
+def run_xgpu(args):
+    """--xgpu G (NEXT-4): the cross-GPU stripe layout, the strips of each stripe
+    spread over G ranks (xgpu.py).  One step = encode (partial + combine) then one recovery
+    (partial + combine) of every stripe.  At --gpus 1 the G ranks are emulated on the one GPU
+    (xgpu.Emulated: each phase is G independent launches over all ranks' data), so the numbers
+    are HBM-only: the NVLink transfer of the partial syndromes (peer stores) is not exercised.
+    Under torchrun (world > 1) each rank is a GPU (xgpu.Distributed, CUDA IPC + NCCL barrier)."""
+    import torch
+    import torch.distributed as dist
+    from paper_cs_0611109_b200 import raid6c as R
+    from paper_cs_0611109_b200 import shard, xgpu
+
+    rank, world, local = _env_rank()
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group(args.dist_backend, device_id=dev if args.dist_backend == "nccl" else None)
+    c = CONFIGS[args.config]
+    p, N = args.prime or c["p"], args.data_strips or c["N"]
+    nbytes = args.strip_bytes or c["nbytes"]
+    S = args.stripes or c["stripes"]
+    G = world if world > 1 else args.xgpu
+    pb = R.parity_bytes(p, nbytes)
+    stream = torch.cuda.Stream(device=dev)
+    plan = R.Plan(p, N, nbytes, local, stream)
+    pairs = pair_schedule(4 if args.config == 4 else 2, N, S, 0, 0)
+    pair_dev = torch.tensor(pairs, dtype=torch.int32, device=dev)
+    if world == 1:
+        ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
+        data = torch.empty((S, N, ss), dtype=torch.uint8, device=dev)
+        par = torch.zeros((S, 2, ps), dtype=torch.uint8, device=dev)
+        R.fill(data, ss, N * ss, nbytes, N, S, 0, args.config, 0, 0, c["sparse"], stream)
+        X = xgpu.Emulated(plan, G, data, par, S)
+
+        def phase(which, er):
+            for r in range(G):
+                (X.partial if which == 0 else X.combine)(r, er)
+    else:
+        X = xgpu.Distributed(plan, S, local, backend=args.dist_backend)
+        k_lo, k_hi = X.blocks[rank]
+        for k in range(k_lo, min(k_hi, N)):
+            R.fill(X.strip_addr(k), 0, X.ss, nbytes, 1, S, 0, args.config, 0, k, c["sparse"], stream)
+
+        def phase(which, er):
+            if which == 0:
+                X.plan.partial_strided([a if k_lo <= k < k_hi else None for k, a in enumerate(X.strips)], X.ss, X.ps,
+                                       S, er, k_lo, k_hi, [X.slot(g, rank, 0) for g in range(G)],
+                                       [X.slot(g, rank, 1) for g in range(G)], X.pstride, X.range)
+            else:
+                lo, hi = X.ranges[rank]
+                if hi > lo:
+                    X.plan.combine_strided(X.strips, X.ss, X.ps, S, er, [X.slot(rank, r, 0) for r in range(G)],
+                                           [X.slot(rank, r, 1) for r in range(G)], X.pstride, lo, hi)
+            X.barrier(stream)
+    torch.cuda.synchronize(dev)
+    total = args.warmup + args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(total)]
+
+    def step(t):
+        with torch.cuda.stream(stream):
+            ev[t][0].record(stream)
+            phase(0, None)
+            ev[t][1].record(stream)
+            phase(1, None)
+            ev[t][2].record(stream)
+            phase(0, pair_dev)
+            ev[t][3].record(stream)
+            phase(1, pair_dev)
+            ev[t][4].record(stream)
+
+    for t in range(args.warmup):
+        step(t)
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = R.launch_count()
+    for t in range(args.warmup, total):
+        step(t)
+    stream.synchronize()
+    launches = R.launch_count() - launches0
+    clk = clocks.stop()
+    ms = [[ev[t][i].elapsed_time(ev[t][i + 1]) for i in range(4)] for t in range(args.warmup, total)]
+    mean = [statistics.mean(m[i] for m in ms) for i in range(4)]
+    mean = [shard.max_over_ranks(v, dev) for v in mean]
+    step_ms = sum(mean)
+    # verification (emulation): the layout's P, Q equal the single-GPU encode's, and the recovered
+    # strips equal the stripes before the step (recovery in place of intact strips)
+    verified = None
+    if world == 1:
+        ref = par.clone()
+        plan.encode_strided(int(data.data_ptr()), X.ss, N * X.ss, int(par.data_ptr()), int(par.data_ptr()) + X.ps,
+                            2 * X.ps, S)
+        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize(dev)
+        R.count_mismatch(par, ref, par.numel(), cnt, stream)
+        dref = data.clone()
+        torch.cuda.synchronize(dev)
+        for s, (x, y) in enumerate(pairs):
+            for k in (x, y):
+                (data[s, k, :nbytes] if k < N else par[s, k - N, :pb]).fill_(0xA5)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            phase(0, pair_dev)
+            phase(1, pair_dev)
+        R.count_mismatch(data, dref, data.numel(), cnt, stream)
+        R.count_mismatch(par, ref, par.numel(), cnt, stream)
+        stream.synchronize()
+        verified = {"mismatched_bytes_vs_single_gpu_path": int(cnt.item())}
+    # algorithmic bytes per phase (all G ranks): partial = every surviving strip read once + G
+    # partial pairs written; combine = G partial pairs read + 2 rebuilt strips written
+    enc_part = S * (N * nbytes + 2 * G * pb)
+    comb = S * (2 * G * pb + 2 * pb)
+    rec_part = sum(N * nbytes + 2 * pb - ((nbytes if x < N else pb) + (nbytes if y < N else pb)) + 2 * G * pb
+                   for (x, y) in pairs)
+    rec_comb = sum(2 * G * pb + (nbytes if x < N else pb) + (nbytes if y < N else pb) for (x, y) in pairs)
+    alg = [enc_part, comb, rec_part, rec_comb]
+    peak, peak_src = measured_peak()
+    names = ["encode_partial", "encode_combine", "recover_partial", "recover_combine"]
+    kern = {nm: {"alg_bytes_all_ranks": a, "avg_ms": round(m, 4),
+                 "achieved_GBps": round(a / (m / 1e3) / 1e9 / (1 if world == 1 else world), 1),
+                 "frac_of_peak": round(a / (m / 1e3) / 1e9 / (1 if world == 1 else world) / peak, 4)}
+            for nm, a, m in zip(names, alg, mean)}
+    dom = max(range(4), key=lambda i: mean[i])
+    user = 2 * S * N * nbytes
+    line = {"metric": "cross-GPU stripe layout (NEXT-4): encode + recover GB/s of user data", "value":
+            round(user / (step_ms / 1e3) / 1e9, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(step_ms, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32 (bitwise GF(2) words)",
+            "data": "synthetic (device generator)",
+            "config": {"workload": f"{c['desc']} with each stripe's strips spread over {G} ranks"
+                                   + (" (emulated on one GPU: HBM only, no NVLink)" if world == 1 else ""),
+                       "p": p, "N": N, "strip_bytes": nbytes, "stripes": S, "ranks": G,
+                       "range_bytes": X.range, "emulated": world == 1},
+            "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": kern[names[dom]]["achieved_GBps"],
+                         "peak": peak, "unit": "GB/s", "frac": kern[names[dom]]["frac_of_peak"],
+                         "peak_source": peak_src},
+            "kernels": kern, "gpu_launches": launches, "clocks": clk, "verified": verified}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        X.close()
+        dist.barrier()
+        dist.destroy_process_group()
+    plan.close()
+
+
 def run_sweep(args):
     """--sweep (config 3, BASELINE.json configs[2]): encode-only write-throughput sweep over strip
     sizes 64 KiB -> 16 MiB (x2 steps, 9 points), each point >= 4 GiB of user data
@@ -773,6 +923,8 @@ def main():
     ap.add_argument("--full", action="store_true",
                     help="whole config (c4: 4096, c5: 1000, c2: 256 stripes) block-sharded over the ranks, "
                          "streamed in waves (strong scaling); --stripes overrides the total")
+    ap.add_argument("--xgpu", type=int, default=0,
+                    help="NEXT-4: spread each stripe's strips over G ranks (emulated on one GPU at --gpus 1)")
     ap.add_argument("--sweep", action="store_true", help="config 3 strip-size sweep 64 KiB -> 16 MiB")
     ap.add_argument("--no-verify", dest="verify", action="store_false")
     ap.add_argument("--no-oracle-check", dest="oracle_check", action="store_false")
@@ -793,6 +945,8 @@ def main():
         run_next1(args)
     elif args.full:
         run_full(args)
+    elif args.xgpu:
+        run_xgpu(args)
     elif args.sweep:
         run_sweep(args)
     else:

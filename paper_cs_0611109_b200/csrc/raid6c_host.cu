@@ -219,8 +219,7 @@ struct raid6c_plan_s {
   cudaStream_t stream = nullptr;
   const zp::FastEntry* fe = nullptr;
   int num_sms = 148;
-  int occ[5] = {1, 1, 1, 1, 1};  // CTAs per SM per kernel mode
-  int occ_combine = 1;          // NEXT-4 combine kernel
+  int occ[6] = {1, 1, 1, 1, 1, 1};  // CTAs per SM per kernel mode
   bool ext = false;           // N > p: extended code of Eq. (qext)
   std::mutex mu;              // serialises the shared single-stripe plans' program buffer
   zp::ExtProg* d_prog = nullptr;
@@ -280,15 +279,12 @@ raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, 
   if (pl->fe && pl->ext && !pl->fe->kernel_ext[0]) pl->fe = nullptr;  // no fast extended kernels: generic
   if (pl->fe) {
     DeviceGuard g(device);
-    for (int m = 0; m < 5; m++) {
+    for (int m = 0; m < 6; m++) {
       const void* k = pl->ext ? pl->fe->kernel_ext[m] : pl->fe->kernel[m];
       const size_t sm = pl->ext ? pl->fe->smem_ext[m] : pl->fe->smem_bytes[m];
       raid6c_status st = kernel_occupancy(device, k, pl->fe->threads + 32, sm, &pl->occ[m]);
       if (st != RAID6C_OK) return st;
     }
-    raid6c_status st = kernel_occupancy(device, pl->ext ? pl->fe->combine_ext : pl->fe->combine,
-                                        pl->fe->combine_threads, pl->fe->combine_smem, &pl->occ_combine);
-    if (st != RAID6C_OK) return st;
   }
   return RAID6C_OK;
 }
@@ -330,9 +326,19 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
       if (a.num_stripes > 1) aligned &= a.part_stride % 16 == 0;
     }
     const uint64_t TB = static_cast<uint64_t>(fe->tile_bytes), CB = static_cast<uint64_t>(fe->chunk_bytes);
-    a.body_tiles = aligned ? pl->bytes / TB : 0;
-    const uint64_t body_end = a.body_tiles * TB;
-    a.tail_units_per_stripe = (pl->pbytes - body_end + CB - 1) / CB;
+    if (mode == zp::KMODE_COMBINE) {
+      // tiles counted from range_lo; a body tile must fit every output (data strips: `bytes`)
+      for (int r = 0; r < a.nsrc; r++)
+        aligned &= ((reinterpret_cast<uintptr_t>(a.src_p[r]) | reinterpret_cast<uintptr_t>(a.src_q[r])) & 15u) == 0;
+      if (a.num_stripes > 1) aligned &= a.part_stride % 16 == 0;
+      const uint64_t lim = std::min<uint64_t>(a.range_hi, pl->bytes);
+      a.body_tiles = (aligned && lim > a.range_lo) ? (lim - a.range_lo) / TB : 0;
+      a.tail_units_per_stripe = (a.range_hi - a.range_lo - a.body_tiles * TB + CB - 1) / CB;
+    } else {
+      a.body_tiles = aligned ? pl->bytes / TB : 0;
+      const uint64_t body_end = a.body_tiles * TB;
+      a.tail_units_per_stripe = (pl->pbytes - body_end + CB - 1) / CB;
+    }
     const uint64_t items = a.body_tiles * static_cast<uint64_t>(a.num_stripes);
     const uint64_t tail_ctas =
         (a.tail_units_per_stripe * static_cast<uint64_t>(a.num_stripes) + fe->threads - 1) / fe->threads;
@@ -381,28 +387,7 @@ raid6c_status strided_args(raid6c_plan pl, const uint8_t* data, size_t strip_str
 // NEXT-4 combine + solve over bytes [a.range_lo, a.range_hi) of every stripe.
 raid6c_status launch_combine(raid6c_plan pl, zp::ZpArgs& a, cudaStream_t st) {
   if (a.num_stripes == 0 || a.range_hi <= a.range_lo) return RAID6C_OK;
-  a.N = pl->N;
-  a.bytes = pl->bytes;
-  a.pbytes = pl->pbytes;
-  cudaError_t err;
-  if (pl->fe) {
-    const zp::FastEntry* fe = pl->fe;
-    const uint64_t units = (a.range_hi - a.range_lo + fe->chunk_bytes - 1) / fe->chunk_bytes;
-    const uint64_t need = (units * static_cast<uint64_t>(a.num_stripes) + fe->combine_threads - 1) / fe->combine_threads;
-    uint64_t grid = std::min<uint64_t>(static_cast<uint64_t>(pl->num_sms) * pl->occ_combine, need);
-    if (grid == 0) grid = 1;
-    void* args[] = {&a};
-    err = cudaLaunchKernel(pl->ext ? fe->combine_ext : fe->combine, dim3(static_cast<unsigned>(grid)),
-                           dim3(fe->combine_threads), args, fe->combine_smem, st);
-  } else {
-    err = zp::generic_launch(a, pl->p, zp::KMODE_COMBINE, st, pl->num_sms);
-  }
-  if (err != cudaSuccess) {
-    pl->sticky = RAID6C_E_CUDA;
-    return cuda_fail(err);
-  }
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return RAID6C_OK;
+  return launch(pl, a, zp::KMODE_COMBINE, st);
 }
 
 // Word-range granule of p's kernels: a TMA tile (fast path) or lcm(byte group, 16) (generic).

@@ -71,14 +71,11 @@ struct FastEntry {
   int chunk_bytes;  // bytes per thread-chunk (whole periods of lcm(n,32) bits)
   int tile_bytes;   // TMA row bytes = consumer threads * chunk_bytes
   int threads;      // consumer threads (+32 producer threads per CTA)
-  const void* kernel[5];  // __global__ void(ZpArgs) per mode: encode, recover, scrub, update, partial
-  size_t smem_bytes[5];
-  const void* kernel_ext[5];  // extended-code (N > p) kernels, nullptr if p fails Theorem 25.3
-  size_t smem_ext[5];
-  const void* combine;      // NEXT-4 combine + solve kernel (basic code)
-  const void* combine_ext;  // (extended code; nullptr if p fails Theorem 25.3)
-  size_t combine_smem;
-  int combine_threads;
+  // __global__ void(ZpArgs) per mode: encode, recover, scrub, update, partial, combine (NEXT-4)
+  const void* kernel[6];
+  size_t smem_bytes[6];
+  const void* kernel_ext[6];  // extended-code (N > p) kernels, nullptr if p fails Theorem 25.3
+  size_t smem_ext[6];
 };
 
 const FastEntry* fast_entry(int p);  // nullptr if p has no fast path

@@ -280,8 +280,10 @@ enum : int { CLS_PQ = 0, CLS_DQ = 1, CLS_DP = 2, CLS_DD = 3, CLS_SCRUB = 4, CLS_
 // Kernel modes (compile-time): the method's two operations and the NEXT-1 pair around them.
 // MODE_PARTIAL (NEXT-4): the fold of a recovery (or encode) restricted to the strips held by one
 // rank, stored unsolved as partial syndromes (dP_r, dQ_r) into the word-range owners' slots.
-enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3, MODE_PARTIAL = 4 };
-constexpr int NUM_MODES = 5;
+// MODE_COMBINE (NEXT-4): the owner of a word range folds the 2*nsrc partial rows of its slots
+// (row 2r = dP_r, row 2r+1 = dQ_r, already reduced) and runs the recovery epilogue.
+enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3, MODE_PARTIAL = 4, MODE_COMBINE = 5 };
+constexpr int NUM_MODES = 6;
 constexpr int K_NEW = -1;     // row index of the update's new-data buffer
 constexpr int K_PART_P = -2;  // partial-mode outputs (slots of the word-range owners)
 constexpr int K_PART_Q = -3;
@@ -308,7 +310,7 @@ __device__ __forceinline__ ItemDesc item_desc(const ZpArgs& a, int s) {
     return d;
   } else {
     int i = a.N, j = a.N + 1;
-    if constexpr (MODE == MODE_RECOVER || MODE == MODE_PARTIAL) {
+    if constexpr (MODE == MODE_RECOVER || MODE == MODE_PARTIAL || MODE == MODE_COMBINE) {
       if (a.er) {
         const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
         i = e.x; j = e.y;
@@ -333,6 +335,7 @@ __device__ __forceinline__ int num_rows(const ZpArgs& a, const ItemDesc& d) {
   // the surviving strips held by this rank: global indices [k_lo, k_hi) minus the lost pair
   else if constexpr (MODE == MODE_PARTIAL)
     return a.k_hi - a.k_lo - (d.x >= a.k_lo && d.x < a.k_hi) - (d.y >= a.k_lo && d.y < a.k_hi);
+  else if constexpr (MODE == MODE_COMBINE) return 2 * a.nsrc;  // (dP_r, dQ_r) per source rank
   // old d_k, new d_k, P, Q: the count (4) comes from the launch args so that the compiler keeps
   // the row loop rolled (a compile-time 4 unrolls it and spills the accumulators)
   else if constexpr (MODE == MODE_UPDATE) return a.upd_rows;
@@ -374,6 +377,18 @@ __device__ __forceinline__ const uint8_t* row_ptr(const ZpArgs& a, int k, int s)
 __device__ __forceinline__ uint64_t row_len(const ZpArgs& a, int k) {
   return (k >= 0 && k < a.N) ? a.bytes : a.pbytes;
 }
+// Address of tile/chunk offset `off` of source row r (combine: offset inside the word range of
+// the partial slot of source r/2; other modes: offset inside strip row_strip(r)).
+template <int MODE>
+__device__ __forceinline__ const uint8_t* in_ptr(const ZpArgs& a, int r, const ItemDesc& d, int s, uint64_t off) {
+  if constexpr (MODE == MODE_COMBINE) {
+    const uint8_t* base = (r & 1) ? a.src_q[r >> 1] : a.src_p[r >> 1];
+    return base + static_cast<uint64_t>(s) * a.part_stride + off;
+  } else {
+    return row_ptr(a, row_strip<MODE>(a, r, d), s) + off;
+  }
+}
+
 // Output address of byte `off` of output strip k of stripe s (partial outputs: the slot of the
 // owner of the word range containing `off`; ranges are whole tiles, so a tile has one owner).
 __device__ __forceinline__ uint8_t* out_ptr(const ZpArgs& a, int k, int s, uint64_t off) {
@@ -416,6 +431,18 @@ __device__ __forceinline__ void fold_row(const ZpArgs& a, const ItemDesc& d, int
       if (amt < 0) amt += G::P;
       rot_acc<G>(L, amt, mtab, acc);
     }
+  }
+}
+
+// Combine fold: row 2r is source r's dP part, row 2r+1 its dQ part (reduced words: rotation 0).
+template <class G>
+__device__ __forceinline__ void fold_partial(int r, const uint32_t (&L)[G::C], uint32_t (&Pa)[G::C], Acc<G>& acc) {
+  if (r & 1) {
+#pragma unroll
+    for (int l = 0; l < G::C; l++) acc.ay[l] ^= L[l];
+  } else {
+#pragma unroll
+    for (int l = 0; l < G::C; l++) Pa[l] ^= L[l];
   }
 }
 
@@ -674,6 +701,10 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
   using G = Geo<P>;
   using LY = Layout<P, MODE>;
   constexpr int C = G::C, CB = G::CB, TB = G::TB, NT = G::THREADS, ST = LY::STAGES, NOUT = LY::NOUT;
+  // the combine runs the recovery epilogue on its folded partials; its tiles are counted from the
+  // start of its word range (obase = range_lo), every other mode's from the start of the strip
+  constexpr int EMODE = MODE == MODE_COMBINE ? MODE_RECOVER : MODE;
+  const uint64_t obase = MODE == MODE_COMBINE ? a.range_lo : 0;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint8_t* outb = smem + (size_t)ST * TB;
@@ -707,7 +738,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
         const ItemDesc d = item_desc<MODE, EXT>(a, s);
         const int R = num_rows<MODE>(a, d);
         for (int r = 0; r < R; r++) {
-          const uint8_t* g = row_ptr(a, row_strip<MODE>(a, r, d), s) + t * TB;
+          const uint8_t* g = in_ptr<MODE>(a, r, d, s, t * TB);
           mbar_wait(&empty[stage], ph ^ 1u);
           mbar_expect_tx(&full[stage], TB);
           tma_load_row(stages + (size_t)stage * TB, g, TB, &full[stage]);
@@ -736,17 +767,21 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
       named_bar_sync(1, NT);
     }
     for (int r = 0; r < R; r++) {
-      int k = row_strip<MODE>(a, r, d);
       uint32_t L[C];
       mbar_wait(&full[stage], ph);
       ld_chunk_smem<C>(stages + (size_t)stage * TB + tid * CB, L);
-      if constexpr (MODE == MODE_UPDATE) {
-        if (k == K_NEW) {
-          k = d.x;  // the new data folds in like the strip it replaces
-          st_chunk_smem<C>(outb + 2 * TB + tid * CB, L);
+      if constexpr (MODE == MODE_COMBINE) {
+        fold_partial<G>(r, L, Pa, acc);
+      } else {
+        int k = row_strip<MODE>(a, r, d);
+        if constexpr (MODE == MODE_UPDATE) {
+          if (k == K_NEW) {
+            k = d.x;  // the new data folds in like the strip it replaces
+            st_chunk_smem<C>(outb + 2 * TB + tid * CB, L);
+          }
         }
+        fold_row<G, EXT>(a, d, k, L, mtab, Pa, acc);
       }
-      fold_row<G, EXT>(a, d, k, L, mtab, Pa, acc);
       // Release the stage only after every loaded lane has been consumed: an mbarrier.arrive
       // issued right after the LDS does not wait for the loads to complete, and the producer's
       // next TMA write (async proxy) can then overwrite the row under a lagging warp's reads.
@@ -756,7 +791,7 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
     }
     uint32_t o0[C], o1[C];
     int k0 = 0, k1 = 0, k2 = 0;
-    epilogue<MODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+    epilogue<EMODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
     if constexpr (NOUT > 0) {
       if constexpr (MODE != MODE_UPDATE) {  // (update waited at the start of the item)
         if (tid == 0) bulk_wait_read0();  // previous item's bulk stores have read outb
@@ -767,9 +802,10 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
       fence_proxy_async_smem();
       named_bar_sync(1, NT);
       if (tid == 0) {
-        tma_store_row(out_ptr(a, k0, s, t * TB), outb, TB);
-        tma_store_row(out_ptr(a, k1, s, t * TB), outb + TB, TB);
-        if constexpr (NOUT == 3) tma_store_row(out_ptr(a, k2, s, t * TB), outb + 2 * TB, TB);
+        const uint64_t ob = obase + t * TB;
+        tma_store_row(out_ptr(a, k0, s, ob), outb, TB);
+        tma_store_row(out_ptr(a, k1, s, ob), outb + TB, TB);
+        if constexpr (NOUT == 3) tma_store_row(out_ptr(a, k2, s, ob), outb + 2 * TB, TB);
         bulk_commit();
       }
     }
@@ -782,7 +818,8 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
   for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * NT + tid; u < tail_total;
        u += static_cast<uint64_t>(gridDim.x) * NT) {
     const int s = static_cast<int>(u / tups);
-    const uint64_t off = body_end + (u - static_cast<uint64_t>(s) * tups) * CB;
+    const uint64_t roff = body_end + (u - static_cast<uint64_t>(s) * tups) * CB;  // row offset
+    const uint64_t off = obase + roff;                                           // strip offset
     const ItemDesc d = item_desc<MODE, EXT>(a, s);
     const int R = num_rows<MODE>(a, d);
     uint32_t Pa[C];
@@ -793,76 +830,35 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
     for (int l = 0; l < C; l++) Pa[l] = 0;
 #pragma unroll 1
     for (int r = 0; r < R; r++) {
-      int k = row_strip<MODE>(a, r, d);
       uint32_t L[C];
-      ld_chunk_global<C>(row_ptr(a, k, s) + off, off, row_len(a, k), L);
-      if constexpr (MODE == MODE_UPDATE) {
-        if (k == K_NEW) {  // old d_k (row 0) of this chunk is already folded: overwrite it now
-          k = d.x;
-          st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k, s)) + off, off, row_len(a, k), L);
+      if constexpr (MODE == MODE_COMBINE) {
+        ld_chunk_global<C>(in_ptr<MODE>(a, r, d, s, roff), off, a.pbytes, L);
+        fold_partial<G>(r, L, Pa, acc);
+        continue;
+      } else {
+        int k = row_strip<MODE>(a, r, d);
+        ld_chunk_global<C>(row_ptr(a, k, s) + off, off, row_len(a, k), L);
+        if constexpr (MODE == MODE_UPDATE) {
+          if (k == K_NEW) {  // old d_k (row 0) of this chunk is already folded: overwrite it now
+            k = d.x;
+            st_chunk_global<C>(const_cast<uint8_t*>(row_ptr(a, k, s)) + off, off, row_len(a, k), L);
+          }
         }
+        fold_row<G, EXT>(a, d, k, L, mtab, Pa, acc);
       }
-      fold_row<G, EXT>(a, d, k, L, mtab, Pa, acc);
     }
     uint32_t o0[C], o1[C];
     int k0 = 0, k1 = 0, k2 = 0;
     if constexpr (MODE == MODE_SCRUB) {  // lanes of a warp may work on different stripes here
       epilogue<MODE, G, false, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
     } else {
-      epilogue<MODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+      epilogue<EMODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
       st_chunk_global<C>(out_ptr(a, k0, s, off), off, row_len(a, k0), o0);
       st_chunk_global<C>(out_ptr(a, k1, s, off), off, row_len(a, k1), o1);
     }
   }
   if constexpr (NOUT > 0)
     if (tid == 0) bulk_wait0();
-}
-
-// ------------------------------------------------------------------ NEXT-4 combine + solve
-// Owner of word range [range_lo, range_hi): sum the nsrc partial syndromes of the range (its own
-// slots, or peer pointers over NVLink) and run the class epilogue of the recovery (encode = PQ)
-// in the same pass, storing the rebuilt strips straight to their owners (a.base[k], possibly
-// peer memory).  One thread per chunk; the solve is identical to zp_kernel's epilogue.
-constexpr int COMBINE_THREADS = 256;
-
-template <int P, bool EXT = false>
-__global__ void __launch_bounds__(COMBINE_THREADS) zp_combine_kernel(const __grid_constant__ ZpArgs a) {
-  using G = Geo<P>;
-  constexpr int C = G::C, CB = G::CB;
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint2* mtab = reinterpret_cast<uint2*>(smem);
-  build_mtab<G>(mtab);
-  __syncthreads();
-  const uint64_t units = (a.range_hi - a.range_lo + CB - 1) / CB;
-  const uint64_t total = units * static_cast<uint64_t>(a.num_stripes);
-  for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
-       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const int s = static_cast<int>(u / units);
-    const uint64_t roff = (u - static_cast<uint64_t>(s) * units) * CB;  // offset inside the range
-    const uint64_t off = a.range_lo + roff;                               // offset inside the strip
-    const ItemDesc d = item_desc<MODE_RECOVER, EXT>(a, s);
-    uint32_t Pa[C], NEW[C];
-    Acc<G> acc;
-    acc.zero();
-#pragma unroll
-    for (int l = 0; l < C; l++) Pa[l] = 0;
-    const uint64_t so = static_cast<uint64_t>(s) * a.part_stride + roff;
-#pragma unroll 1
-    for (int r = 0; r < a.nsrc; r++) {
-      uint32_t L[C];
-      ld_chunk_global<C>(a.src_p[r] + so, off, a.pbytes, L);
-#pragma unroll
-      for (int l = 0; l < C; l++) Pa[l] ^= L[l];
-      ld_chunk_global<C>(a.src_q[r] + so, off, a.pbytes, L);
-#pragma unroll
-      for (int l = 0; l < C; l++) acc.ay[l] ^= L[l];  // reduced words: rotation by 0
-    }
-    uint32_t o0[C], o1[C];
-    int k0 = 0, k1 = 0, k2 = 0;
-    epilogue<MODE_RECOVER, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
-    st_chunk_global<C>(out_ptr(a, k0, s, off), off, row_len(a, k0), o0);
-    st_chunk_global<C>(out_ptr(a, k1, s, off), off, row_len(a, k1), o1);
-  }
 }
 
 template <int P, bool WITH_EXT>
@@ -879,9 +875,8 @@ FastEntry make_entry() {
   e.kernel[MODE_UPDATE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_UPDATE>);
   e.kernel[MODE_PARTIAL] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_PARTIAL>);
   e.smem_bytes[MODE_PARTIAL] = Layout<P, MODE_PARTIAL>::SMEM;
-  e.combine = reinterpret_cast<const void*>(&zp_combine_kernel<P, false>);
-  e.combine_smem = static_cast<size_t>(G::MTAB) * 8;
-  e.combine_threads = COMBINE_THREADS;
+  e.kernel[MODE_COMBINE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_COMBINE>);
+  e.smem_bytes[MODE_COMBINE] = Layout<P, MODE_COMBINE>::SMEM;
   e.smem_bytes[MODE_ENCODE] = Layout<P, MODE_ENCODE>::SMEM;
   e.smem_bytes[MODE_RECOVER] = Layout<P, MODE_RECOVER>::SMEM;
   e.smem_bytes[MODE_SCRUB] = Layout<P, MODE_SCRUB>::SMEM;
@@ -893,7 +888,8 @@ FastEntry make_entry() {
     e.kernel_ext[MODE_UPDATE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_UPDATE, true>);
     e.kernel_ext[MODE_PARTIAL] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_PARTIAL, true>);
     e.smem_ext[MODE_PARTIAL] = Layout<P, MODE_PARTIAL>::SMEM;
-    e.combine_ext = reinterpret_cast<const void*>(&zp_combine_kernel<P, true>);
+    e.kernel_ext[MODE_COMBINE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_COMBINE, true>);
+    e.smem_ext[MODE_COMBINE] = Layout<P, MODE_COMBINE>::SMEM;
     e.smem_ext[MODE_ENCODE] = Layout<P, MODE_ENCODE>::SMEM;
     e.smem_ext[MODE_RECOVER] = Layout<P, MODE_RECOVER>::SMEM;
     e.smem_ext[MODE_SCRUB] = Layout<P, MODE_SCRUB>::SMEM;
@@ -913,7 +909,7 @@ FastEntry make_entry() {
   template __global__ void zp_kernel<PP, MODE_SCRUB>(const __grid_constant__ ZpArgs);         \
   template __global__ void zp_kernel<PP, MODE_UPDATE>(const __grid_constant__ ZpArgs);        \
   template __global__ void zp_kernel<PP, MODE_PARTIAL>(const __grid_constant__ ZpArgs);       \
-  template __global__ void zp_combine_kernel<PP, false>(const __grid_constant__ ZpArgs);      \
+  template __global__ void zp_kernel<PP, MODE_COMBINE>(const __grid_constant__ ZpArgs);       \
   const FastEntry* fast_entry_##PP() {                                                       \
     static const FastEntry e = make_entry<PP, WITH_EXT>();                                   \
     return &e;                                                                               \
@@ -927,6 +923,6 @@ FastEntry make_entry() {
   template __global__ void zp_kernel<PP, MODE_SCRUB, true>(const __grid_constant__ ZpArgs);   \
   template __global__ void zp_kernel<PP, MODE_UPDATE, true>(const __grid_constant__ ZpArgs);  \
   template __global__ void zp_kernel<PP, MODE_PARTIAL, true>(const __grid_constant__ ZpArgs); \
-  template __global__ void zp_combine_kernel<PP, true>(const __grid_constant__ ZpArgs);       \
+  template __global__ void zp_kernel<PP, MODE_COMBINE, true>(const __grid_constant__ ZpArgs); \
   }                                                                                          \
   ZP_INSTANTIATE_FAST_IMPL(PP, true)
