@@ -49,12 +49,18 @@ struct Geo {
   static constexpr int P = P_;
   static constexpr int n = P - 1;
   static constexpr int LAMBDA = n / cgcd(n, 32);  // 32-bit lanes per period lcm(n,32)
-  static constexpr int C = LAMBDA < 12 ? LAMBDA * (12 / LAMBDA) : LAMBDA;  // lanes per chunk
+#ifdef ZP_C8
+  // experiment: lane-aligned small words (n | 32) in 32-byte chunks, 256 threads, 8 KiB tiles
+  static constexpr bool SMALL8 = (32 % n == 0);
+#else
+  static constexpr bool SMALL8 = false;
+#endif
+  static constexpr int C = SMALL8 ? 8 : (LAMBDA < 12 ? LAMBDA * (12 / LAMBDA) : LAMBDA);  // lanes per chunk
   static constexpr int CB = 4 * C;                   // chunk bytes
   static constexpr int QMAX = n >> 5;                // max whole-lane shift
   // consumer threads per CTA; 224 for lane-aligned small words (n | 32) so that the 48-byte
   // chunk tiles (10752 B) leave a 1.5% instead of 6% ragged tail on 64 KiB strips (config 1)
-  static constexpr int THREADS = C >= 24 ? 128 : ((32 % n == 0) ? 224 : 256);
+  static constexpr int THREADS = SMALL8 ? 256 : (C >= 24 ? 128 : ((32 % n == 0) ? 224 : 256));
   static constexpr int TB = THREADS * CB;            // TMA row (tile) bytes
   static constexpr int MTAB = (n + 1) * LAMBDA;      // mask table entries (uint2)
   static constexpr int SMEM_TARGET = 112 * 1024;     // 2 CTAs per SM
@@ -374,8 +380,10 @@ __device__ __forceinline__ const uint8_t* row_ptr(const ZpArgs& a, int k, int s)
   return k == K_NEW ? a.nbase + static_cast<uint64_t>(s) * a.new_stride
                     : a.base[k] + static_cast<uint64_t>(s) * strip_stride(a, k);
 }
+// Length of row k: data strips and the update's new-data row are `bytes` long; P, Q and the
+// NEXT-4 partial slots hold parity-format strips (pbytes).
 __device__ __forceinline__ uint64_t row_len(const ZpArgs& a, int k) {
-  return (k >= 0 && k < a.N) ? a.bytes : a.pbytes;
+  return (k == K_NEW || (k >= 0 && k < a.N)) ? a.bytes : a.pbytes;
 }
 // Address of tile/chunk offset `off` of source row r (combine: offset inside the word range of
 // the partial slot of source r/2; other modes: offset inside strip row_strip(r)).

@@ -100,3 +100,28 @@ def test_scrub_counts_match_oracle(p, N, nbytes, S, offset):
     for s in range(S):
         strips = [_np(b.strip(s, k)).copy() for k in range(N + 2)]
         assert got[s] == oracle.count_bad_words(p, N, strips, nbytes), s
+
+
+@pytest.mark.parametrize("p,N,nbytes", [(13, 12, 5000), (13, 16, 4 * 12288 + 1000), (61, 60, 15360 + 9)])
+def test_update_new_data_read_only_to_strip_length(p, N, nbytes):
+    """The new-data row is `bytes` long even when parity strips are longer (R5): with the new rows
+    packed back to back (new_stride == bytes) and 0xFF around them, bytes past each row must not
+    leak into P, Q (a regression: the row was once read to parity length)."""
+    S = 3
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=13, cfg=6)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    assert R.parity_bytes(p, nbytes) > nbytes
+    newbuf = torch.full((S * nbytes + 64,), 0xFF, dtype=torch.uint8, device="cuda")
+    new = newbuf[:S * nbytes].view(S, nbytes)
+    R.fill(new, nbytes, nbytes, nbytes, 1, S, 14, 8, 0, 0, 0)
+    disks = [(5 * s + 2) % N for s in range(S)]
+    plan.update_strided(*b.args(), int(new.data_ptr()), nbytes, torch.tensor(disks, dtype=torch.int32, device="cuda"))
+    plan.sync()
+    for s in range(S):
+        data = synthetic.stripe_strips(13, 6, s, N, nbytes)
+        data[disks[s]] = _np(new[s])
+        P, Q = (oracle.encode_ext if N > p else oracle.encode)(p, data, nbytes)
+        assert np.array_equal(_np(b.strip(s, N)), P), s
+        assert np.array_equal(_np(b.strip(s, N + 1)), Q), s
