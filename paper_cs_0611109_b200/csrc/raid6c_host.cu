@@ -282,7 +282,7 @@ raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, 
     for (int m = 0; m < 6; m++) {
       const void* k = pl->ext ? pl->fe->kernel_ext[m] : pl->fe->kernel[m];
       const size_t sm = pl->ext ? pl->fe->smem_ext[m] : pl->fe->smem_bytes[m];
-      raid6c_status st = kernel_occupancy(device, k, pl->fe->threads + 32, sm, &pl->occ[m]);
+      raid6c_status st = kernel_occupancy(device, k, pl->fe->threads[m] + 32, sm, &pl->occ[m]);
       if (st != RAID6C_OK) return st;
     }
   }
@@ -325,7 +325,8 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
         aligned &= ((reinterpret_cast<uintptr_t>(a.part_p[g]) | reinterpret_cast<uintptr_t>(a.part_q[g])) & 15u) == 0;
       if (a.num_stripes > 1) aligned &= a.part_stride % 16 == 0;
     }
-    const uint64_t TB = static_cast<uint64_t>(fe->tile_bytes), CB = static_cast<uint64_t>(fe->chunk_bytes);
+    const uint64_t TB = static_cast<uint64_t>(fe->tile_bytes[mode]), CB = static_cast<uint64_t>(fe->chunk_bytes[mode]);
+    const int NT = fe->threads[mode];
     if (mode == zp::KMODE_COMBINE) {
       // tiles counted from range_lo; a body tile must fit every output (data strips: `bytes`)
       for (int r = 0; r < a.nsrc; r++)
@@ -341,13 +342,13 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
     }
     const uint64_t items = a.body_tiles * static_cast<uint64_t>(a.num_stripes);
     const uint64_t tail_ctas =
-        (a.tail_units_per_stripe * static_cast<uint64_t>(a.num_stripes) + fe->threads - 1) / fe->threads;
+        (a.tail_units_per_stripe * static_cast<uint64_t>(a.num_stripes) + NT - 1) / NT;
     const uint64_t cap = static_cast<uint64_t>(pl->num_sms) * pl->occ[mode];
     uint64_t grid = std::min<uint64_t>(cap, std::max<uint64_t>(items, tail_ctas));
     if (grid == 0) grid = 1;
     void* args[] = {&a};
     err = cudaLaunchKernel(pl->ext ? fe->kernel_ext[mode] : fe->kernel[mode], dim3(static_cast<unsigned>(grid)),
-                           dim3(fe->threads + 32), args, pl->ext ? fe->smem_ext[mode] : fe->smem_bytes[mode], st);
+                           dim3(NT + 32), args, pl->ext ? fe->smem_ext[mode] : fe->smem_bytes[mode], st);
   } else {
     err = zp::generic_launch(a, pl->p, mode, st, pl->num_sms);
   }
@@ -392,14 +393,16 @@ raid6c_status launch_combine(raid6c_plan pl, zp::ZpArgs& a, cudaStream_t st) {
 
 // Word-range granule of p's kernels: a TMA tile (fast path) or lcm(byte group, 16) (generic).
 uint64_t range_granule_p(int p) {
-  if (const zp::FastEntry* fe = zp::fast_entry(p)) return static_cast<uint64_t>(fe->tile_bytes);
+  // ranges are whole tiles of the partial kernel (a tile has one owner); the combine kernel
+  // starts its own tiles at each range start (16-byte and word aligned)
+  if (const zp::FastEntry* fe = zp::fast_entry(p)) return static_cast<uint64_t>(fe->tile_bytes[zp::KMODE_PARTIAL]);
   const int n = p - 1;
   const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);
   const uint64_t gb = static_cast<uint64_t>(g) * n / 8;
   return gb * 16 / std::gcd<uint64_t>(gb, 16);
 }
 uint64_t range_granule(raid6c_plan pl) {
-  if (pl->fe) return static_cast<uint64_t>(pl->fe->tile_bytes);
+  if (pl->fe) return static_cast<uint64_t>(pl->fe->tile_bytes[zp::KMODE_PARTIAL]);
   return range_granule_p(pl->p);
 }
 

@@ -68,9 +68,10 @@ struct ZpArgs {
 // instantiation translation unit and used by the host to split work and launch.
 struct FastEntry {
   int p;
-  int chunk_bytes;  // bytes per thread-chunk (whole periods of lcm(n,32) bits)
-  int tile_bytes;   // TMA row bytes = consumer threads * chunk_bytes
-  int threads;      // consumer threads (+32 producer threads per CTA)
+  // per kernel mode (the geometry may differ between modes, see zp_fast.cuh Geo):
+  int chunk_bytes[6];  // bytes per thread-chunk (whole periods of lcm(n,32) bits)
+  int tile_bytes[6];   // TMA row bytes = consumer threads * chunk_bytes
+  int threads[6];      // consumer threads (+32 producer threads per CTA)
   // __global__ void(ZpArgs) per mode: encode, recover, scrub, update, partial, combine (NEXT-4)
   const void* kernel[6];
   size_t smem_bytes[6];

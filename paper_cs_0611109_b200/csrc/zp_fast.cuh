@@ -44,22 +44,22 @@ namespace zp {
 constexpr int cgcd(int a, int b) { return b == 0 ? a : cgcd(b, a % b); }
 constexpr int top_bit(int v) { return v <= 1 ? 0 : 1 + top_bit(v >> 1); }
 
-template <int P_>
+// Chunk / tile geometry of one kernel instantiation.  SMALL8_ selects, for lane-aligned small
+// words (n | 32: p = 3, 5, 17), 32-byte chunks x 256 threads = 8 KiB tiles, which divide
+// power-of-two strips exactly (no ragged tail); it is used by the light-ALU modes (encode,
+// partial: measured +6% on config 1 and +7% for p = 17), while the recovery modes keep 48-byte
+// chunks (fewer per-chunk epilogue overheads per byte: C8 measured -10% there).
+template <int P_, bool SMALL8_ = false>
 struct Geo {
   static constexpr int P = P_;
   static constexpr int n = P - 1;
   static constexpr int LAMBDA = n / cgcd(n, 32);  // 32-bit lanes per period lcm(n,32)
-#ifdef ZP_C8
-  // experiment: lane-aligned small words (n | 32) in 32-byte chunks, 256 threads, 8 KiB tiles
-  static constexpr bool SMALL8 = (32 % n == 0);
-#else
-  static constexpr bool SMALL8 = false;
-#endif
+  static constexpr bool SMALL8 = SMALL8_ && (32 % n == 0);
   static constexpr int C = SMALL8 ? 8 : (LAMBDA < 12 ? LAMBDA * (12 / LAMBDA) : LAMBDA);  // lanes per chunk
   static constexpr int CB = 4 * C;                   // chunk bytes
   static constexpr int QMAX = n >> 5;                // max whole-lane shift
-  // consumer threads per CTA; 224 for lane-aligned small words (n | 32) so that the 48-byte
-  // chunk tiles (10752 B) leave a 1.5% instead of 6% ragged tail on 64 KiB strips (config 1)
+  // consumer threads per CTA; 224 for lane-aligned small words (n | 32) with 48-byte chunks so
+  // that the tiles (10752 B) leave a 1.5% instead of 6% ragged tail on 64 KiB strips (config 1)
   static constexpr int THREADS = SMALL8 ? 256 : (C >= 24 ? 128 : ((32 % n == 0) ? 224 : 256));
   static constexpr int TB = THREADS * CB;            // TMA row (tile) bytes
   static constexpr int MTAB = (n + 1) * LAMBDA;      // mask table entries (uint2)
@@ -290,6 +290,9 @@ enum : int { CLS_PQ = 0, CLS_DQ = 1, CLS_DP = 2, CLS_DD = 3, CLS_SCRUB = 4, CLS_
 // (row 2r = dP_r, row 2r+1 = dQ_r, already reduced) and runs the recovery epilogue.
 enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3, MODE_PARTIAL = 4, MODE_COMBINE = 5 };
 constexpr int NUM_MODES = 6;
+// Geometry of mode MODE's kernel for prime P (see Geo).
+template <int P, int MODE>
+using GeoM = Geo<P, MODE == MODE_ENCODE || MODE == MODE_PARTIAL>;
 constexpr int K_NEW = -1;     // row index of the update's new-data buffer
 constexpr int K_PART_P = -2;  // partial-mode outputs (slots of the word-range owners)
 constexpr int K_PART_Q = -3;
@@ -659,7 +662,7 @@ __device__ __forceinline__ void build_mtab(uint2* mtab) {
 // Shared-memory layout per (p, mode): STAGES TMA rows, NOUT output rows, mask table, barriers.
 template <int P, int MODE>
 struct Layout {
-  using G = Geo<P>;
+  using G = GeoM<P, MODE>;
   static constexpr int NOUT = num_outputs<MODE>();
   static constexpr int STAGES_RAW = (G::SMEM_TARGET - NOUT * G::TB - G::MTAB * 8 - 256) / G::TB;
   static constexpr int STAGES = STAGES_RAW < 3 ? 3 : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
@@ -705,8 +708,8 @@ __device__ __forceinline__ void epilogue(const ZpArgs& a, const ItemDesc& d, int
 }
 
 template <int P, int MODE, bool EXT = false>
-__global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __grid_constant__ ZpArgs a) {
-  using G = Geo<P>;
+__global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, 2) zp_kernel(const __grid_constant__ ZpArgs a) {
+  using G = GeoM<P, MODE>;
   using LY = Layout<P, MODE>;
   constexpr int C = G::C, CB = G::CB, TB = G::TB, NT = G::THREADS, ST = LY::STAGES, NOUT = LY::NOUT;
   // the combine runs the recovery epilogue on its folded partials; its tiles are counted from the
@@ -869,14 +872,22 @@ __global__ void __launch_bounds__(Geo<P>::THREADS + 32, 2) zp_kernel(const __gri
     if (tid == 0) bulk_wait0();
 }
 
+template <int P, int M>
+void fill_geo(FastEntry& e) {
+  if constexpr (M < NUM_MODES) {
+    using G = GeoM<P, M>;
+    e.chunk_bytes[M] = G::CB;
+    e.tile_bytes[M] = G::TB;
+    e.threads[M] = G::THREADS;
+    fill_geo<P, M + 1>(e);
+  }
+}
+
 template <int P, bool WITH_EXT>
 FastEntry make_entry() {
-  using G = Geo<P>;
   FastEntry e{};
   e.p = P;
-  e.chunk_bytes = G::CB;
-  e.tile_bytes = G::TB;
-  e.threads = G::THREADS;
+  fill_geo<P, 0>(e);
   e.kernel[MODE_ENCODE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_ENCODE>);
   e.kernel[MODE_RECOVER] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_RECOVER>);
   e.kernel[MODE_SCRUB] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_SCRUB>);
