@@ -359,3 +359,35 @@ def test_pipeline_race_stress(p, N, nbytes, S):
             P, Q = oracle.encode(p, segs, b1 - b0)
             assert np.array_equal(_np(b.par[s, 0, b0:b0 + P.size]), P)
             assert np.array_equal(_np(b.par[s, 1, b0:b0 + Q.size]), Q)
+
+
+@pytest.mark.parametrize("p", [5, 13, 17, 59, 61, 257, 11, 97])
+def test_dd_solve_every_z(p):
+    """The DD solve (1 + x^z)^{-1} (reading R11) for every z = y - x in
+    1..N-1 with N = p - 1 data strips, at varying x (the rotation origin): one stripe per z,
+    batched, through the TMA path with a ragged tail.  The encode of the batch is checked
+    against the oracle first; the rebuilt strips must equal the originals."""
+    N = p - 1
+    nbytes = {5: 10752 + 333, 13: 12288 + 333, 17: 10752 + 77, 59: 14848 + 333, 61: 15360 + 333,
+              257: 8192 + 96, 11: 3000, 97: 2000}[p]
+    zs = list(range(1, N))
+    S = len(zs)
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=41, cfg=17)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    for s in (0, S - 1):
+        data = synthetic.stripe_strips(41, 17, s, N, nbytes)
+        P, Q = oracle.encode(p, data, nbytes)
+        assert np.array_equal(_np(b.strip(s, N)), P) and np.array_equal(_np(b.strip(s, N + 1)), Q)
+    orig = b.data.clone()
+    pairs = []
+    for s, z in enumerate(zs):
+        x = (7 * z + s) % (N - z)
+        pairs.append((x + z, x))  # reversed order: the library canonicalises
+        _poison(b, s, (x, x + z))
+    plan.recover_strided(*b.args(), torch.tensor(pairs, dtype=torch.int32, device="cuda"))
+    plan.sync()
+    bad = (b.data[:, :, :nbytes] != orig[:, :, :nbytes]).nonzero()
+    assert bad.numel() == 0, (p, bad[:5].tolist(), [pairs[int(i)] for i in bad[:5, 0].tolist()])
