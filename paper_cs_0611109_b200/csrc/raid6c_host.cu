@@ -463,6 +463,15 @@ raid6c_status upload_programs(raid6c_plan pl, const std::vector<int2>& pairs, cu
       }
       for (int i = 0; i < p - 1; i++)
         if (u.bit(i)) pr.e[pr.nu++] = static_cast<uint16_t>(i);
+      // u and u + (1 + x + ... + x^{p-1}) are the same element of R_p (the p-th roots of unity
+      // sum to zero, Lemma 24.2), and the kernel multiplies in R' with
+      // deferred reduction: take whichever has fewer terms (the complement includes x^{p-1}).
+      if (2 * pr.nu > p) {
+        int k = 0;
+        for (int i = 0; i < p; i++)
+          if (i == p - 1 || !u.bit(i)) pr.e[k++] = static_cast<uint16_t>(i);
+        pr.nu = k;
+      }
     }
     memo[{x, y}] = s;
   }
