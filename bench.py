@@ -269,7 +269,10 @@ def run_ours(args):
     # ---------------------------------------------------------------- e2e (host buffers, public API)
     e2e = None
     if args.e2e and do_enc and not rs:
-        e2e = run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_lists, do_rec, world, dev)
+        try:
+            e2e = run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_lists, do_rec, world, dev)
+        except (RuntimeError, MemoryError) as exc:  # e.g. pinned host memory exhausted at large N
+            e2e = {"value": None, "unit": "GB/s", "error": f"{type(exc).__name__}: {exc}"[:300]}
 
     user_bytes_step = (int(do_enc) + int(do_rec)) * N * nbytes * S
     value = world * user_bytes_step * args.steps / (elapsed_ms / 1e3) / 1e9
