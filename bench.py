@@ -747,8 +747,15 @@ def run_next1(args):
 def run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_lists, do_rec, world, dev):
     """Same workload through the host-buffer public API (raid6c_encode_host/recover_host):
     H2D of inputs and D2H of results inside the timed region, pinned host memory."""
-    hd = torch.empty((S, N, ss), dtype=torch.uint8).pin_memory()
-    hp = torch.zeros((S, 2, ps), dtype=torch.uint8).pin_memory()
+    from paper_cs_0611109_b200 import shard
+    err = None
+    try:
+        hd = torch.empty((S, N, ss), dtype=torch.uint8).pin_memory()
+        hp = torch.zeros((S, 2, ps), dtype=torch.uint8).pin_memory()
+    except (RuntimeError, MemoryError) as exc:
+        err = f"{type(exc).__name__}: {exc}"[:300]
+    if shard.sum_over_ranks([int(err is not None)], dev)[0]:  # every rank skips if any rank failed
+        raise RuntimeError(err or "pinned host allocation failed on another rank")
     hd.copy_(data)  # device -> pinned host, no pageable temporary
     hd_ptr, hp_ptr = int(hd.data_ptr()), int(hp.data_ptr())
     a = (hd_ptr, ss, N * ss, hp_ptr, hp_ptr + ps, 2 * ps, S)
@@ -772,7 +779,6 @@ def run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_list
             h2d, d2h = b1[0] + b2[0], b1[1] + b2[1]
     # correctness of the host path vs the device path (parity of the same stripes)
     same = bool(torch.equal(hp[:, :, :pb], par[:, :, :pb].cpu()))
-    from paper_cs_0611109_b200 import shard
     tm = shard.max_over_ranks(statistics.mean(times), dev)
     user = (1 + int(do_rec)) * N * nbytes * S * world
     return {"value": round(user / tm / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d,
