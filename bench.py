@@ -244,7 +244,9 @@ def run_ours(args):
     elapsed_ms = t_start.elapsed_time(t_end)
     enc_ms = [ev[t][0].elapsed_time(ev[t][1]) for t in range(args.warmup, total_steps)]
     rec_ms = [ev[t][1].elapsed_time(ev[t][2]) for t in range(args.warmup, total_steps)]
-    elapsed_ms = shard.max_over_ranks(elapsed_ms, dev)
+    per_rank = shard.gather_over_ranks(elapsed_ms, dev)
+    per_rank_ms = [round(x, 3) for x in per_rank]
+    elapsed_ms = max(per_rank)
 
     # ---------------------------------------------------------------- verification
     verified = None
@@ -310,6 +312,7 @@ def run_ours(args):
                    "stripes_per_gpu": S, "ops": ops, "parallelism": f"stripe-sharded x{world} (no data-path collective)",
                    "l2": "working set >= 1 GiB >> 126 MB L2 (no flush needed)"},
         "roofline": roof, "kernels": per_kernel, "gpu_launches": launches, "clocks": clk,
+        "per_rank_ms": per_rank_ms,
         "verified": verified, "e2e": e2e,
         "fast_path": R.has_fast_path(p), "code": args.code,
     }

@@ -44,3 +44,16 @@ def sum_over_ranks(values, device=None) -> list[int]:
     t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return [int(v) for v in t.tolist()]
+
+
+def gather_over_ranks(value: float, device=None) -> list[float]:
+    """Per-rank values of a scalar (e.g. each rank's elapsed ms), in rank order."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [float(value)]
+    dev = _coll_device(device)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    out = [torch.zeros_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [float(x.item()) for x in out]

@@ -44,6 +44,7 @@ def _worker(rank, world, port, total, q):
     dig = _digest_stripes(lo, hi)
     mx = shard.max_over_ranks(10.0 + rank)
     sm = shard.sum_over_ranks([hi - lo, rank + 1])
+    assert shard.gather_over_ranks(10.0 + rank) == [10.0 + r for r in range(world)]
     dist.barrier()
     dist.destroy_process_group()
     q.put((rank, lo, hi, dig, mx, sm))
