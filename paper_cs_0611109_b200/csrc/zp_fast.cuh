@@ -33,11 +33,21 @@
 //   * The ragged end of each strip ([body_tiles*TB, parity_bytes)) is handled by the same
 //     arithmetic with direct, byte-precise global loads and stores (tail units).
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #include "sub_chain.cuh"
 #include "zp_args.h"
+
+// ZP_BOUNDS_CHECK builds (python -m paper_cs_0611109_b200.build -D ZP_BOUNDS_CHECK --out ...)
+// assert that every TMA row load and bulk store stays inside its strip / slot: the stand-in for
+// compute-sanitizer, which is closed on this GPU pool.  Off in the product build.
+#ifdef ZP_BOUNDS_CHECK
+#define ZP_CHECK(cond) assert(cond)
+#else
+#define ZP_CHECK(cond) ((void)0)
+#endif
 
 namespace zp {
 
@@ -750,6 +760,10 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, 2) zp_kernel(cons
         const int R = num_rows<MODE>(a, d);
         for (int r = 0; r < R; r++) {
           const uint8_t* g = in_ptr<MODE>(a, r, d, s, t * TB);
+          // the whole row tile lies inside its strip (combine: inside the slot's range)
+          ZP_CHECK((t + 1) * TB <= (MODE == MODE_COMBINE ? a.range_hi - a.range_lo
+                                                           : row_len(a, row_strip<MODE>(a, r, d))));
+          ZP_CHECK((reinterpret_cast<uintptr_t>(g) & 15u) == 0);
           mbar_wait(&empty[stage], ph ^ 1u);
           mbar_expect_tx(&full[stage], TB);
           tma_load_row(stages + (size_t)stage * TB, g, TB, &full[stage]);
@@ -814,6 +828,12 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, 2) zp_kernel(cons
       named_bar_sync(1, NT);
       if (tid == 0) {
         const uint64_t ob = obase + t * TB;
+        // every stored tile lies inside its output strip (partial: inside one owner's slot)
+        ZP_CHECK(ob + TB <= row_len(a, k0) && ob + TB <= row_len(a, k1));
+        if constexpr (NOUT == 3) ZP_CHECK(ob + TB <= row_len(a, k2));
+        if constexpr (MODE == MODE_PARTIAL)
+          ZP_CHECK(ob / a.range_bytes < static_cast<uint64_t>(a.nranges) &&
+                   ob % a.range_bytes + TB <= a.range_bytes);
         tma_store_row(out_ptr(a, k0, s, ob), outb, TB);
         tma_store_row(out_ptr(a, k1, s, ob), outb + TB, TB);
         if constexpr (NOUT == 3) tma_store_row(out_ptr(a, k2, s, ob), outb + 2 * TB, TB);
