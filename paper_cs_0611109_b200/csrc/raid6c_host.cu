@@ -226,6 +226,10 @@ struct raid6c_plan_s {
   size_t prog_cap = 0;
   int2* d_er = nullptr;
   size_t er_cap = 0;
+  // d_er / d_prog are rewritten by later calls, possibly on another stream (plan_set_stream):
+  // the last launch that reads them records this event, and every rewrite waits for it
+  cudaEvent_t tables_done = nullptr;
+  bool tables_pending = false;
   raid6c_status sticky = RAID6C_OK;
   // host-buffer pipeline
   uint8_t* d_stage = nullptr;
@@ -293,6 +297,7 @@ void plan_release(raid6c_plan pl) {
   DeviceGuard g(pl->device);
   if (pl->d_er) cudaFree(pl->d_er);
   if (pl->d_prog) cudaFree(pl->d_prog);
+  if (pl->tables_done) cudaEventDestroy(pl->tables_done);
   if (pl->d_stage) cudaFree(pl->d_stage);
   for (int i = 0; i < 3; i++)
     if (pl->hs[i]) cudaStreamDestroy(pl->hs[i]);
@@ -305,6 +310,8 @@ void plan_release(raid6c_plan pl) {
 
 // Launch one batch (all stripes share p, N, bytes).  a.base / strides / erasures are set.
 // mode: zp::KMODE_ENCODE / RECOVER / SCRUB / UPDATE.
+raid6c_status tables_after_read(raid6c_plan pl, const zp::ZpArgs& a, cudaStream_t st);
+
 raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
   if (a.num_stripes == 0) return RAID6C_OK;
   a.N = pl->N;
@@ -357,7 +364,7 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
     return cuda_fail(err);
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  return RAID6C_OK;
+  return tables_after_read(pl, a, st);
 }
 
 raid6c_status check_erasure(int N, int i, int j) {
@@ -406,6 +413,35 @@ uint64_t range_granule(raid6c_plan pl) {
   return range_granule_p(pl->p);
 }
 
+// Order a rewrite of the plan's device tables (d_er, d_prog) on stream st after every launch
+// that reads them; `freeing` = the buffer is about to be released (wait on the host instead).
+raid6c_status tables_before_write(raid6c_plan pl, cudaStream_t st, bool freeing) {
+#ifdef ZP_NO_TABLE_ORDER  // negative control for tests/test_gpu_parity.py (never in the product build)
+  return RAID6C_OK;
+#endif
+  if (!pl->tables_pending) return RAID6C_OK;
+  if (freeing) {
+    ZP_CUDA(cudaEventSynchronize(pl->tables_done));
+    pl->tables_pending = false;
+    return RAID6C_OK;
+  }
+  ZP_CUDA(cudaStreamWaitEvent(st, pl->tables_done, 0));
+  return RAID6C_OK;
+}
+
+// After a launch on st whose arguments point into d_er / d_prog.
+raid6c_status tables_after_read(raid6c_plan pl, const zp::ZpArgs& a, cudaStream_t st) {
+  const bool uses_er = pl->d_er && ((a.er >= pl->d_er && a.er < pl->d_er + pl->er_cap) ||
+                                    (reinterpret_cast<const int2*>(a.upd) >= pl->d_er &&
+                                     reinterpret_cast<const int2*>(a.upd) < pl->d_er + pl->er_cap));
+  const bool uses_prog = pl->d_prog && a.prog >= pl->d_prog && a.prog < pl->d_prog + pl->prog_cap;
+  if (!uses_er && !uses_prog) return RAID6C_OK;
+  if (!pl->tables_done) ZP_CUDA(cudaEventCreateWithFlags(&pl->tables_done, cudaEventDisableTiming));
+  ZP_CUDA(cudaEventRecord(pl->tables_done, st));
+  pl->tables_pending = true;
+  return RAID6C_OK;
+}
+
 // Upload host erasure pairs (validated, canonical) into the plan's device buffer.
 raid6c_status upload_erasures(raid6c_plan pl, const raid6c_erasure* er, int count, cudaStream_t st) {
   std::vector<int2> h(count);
@@ -419,6 +455,8 @@ raid6c_status upload_erasures(raid6c_plan pl, const raid6c_erasure* er, int coun
     DeviceGuard g(pl->device);
     if (pl->d_er) {
       ZP_CUDA(cudaStreamSynchronize(st));
+      raid6c_status w = tables_before_write(pl, st, true);
+      if (w != RAID6C_OK) return w;
       cudaFree(pl->d_er);
       pl->d_er = nullptr;
     }
@@ -426,6 +464,8 @@ raid6c_status upload_erasures(raid6c_plan pl, const raid6c_erasure* er, int coun
     ZP_CUDA(cudaMalloc(&pl->d_er, cap * sizeof(int2)));
     pl->er_cap = cap;
   }
+  raid6c_status w = tables_before_write(pl, st, false);
+  if (w != RAID6C_OK) return w;
   // pageable source: the copy is staged before this call returns, so `h` may be freed
   ZP_CUDA(cudaMemcpyAsync(pl->d_er, h.data(), count * sizeof(int2), cudaMemcpyHostToDevice, st));
   return RAID6C_OK;
@@ -479,6 +519,8 @@ raid6c_status upload_programs(raid6c_plan pl, const std::vector<int2>& pairs, cu
     DeviceGuard g(pl->device);
     if (pl->d_prog) {
       ZP_CUDA(cudaStreamSynchronize(st));
+      raid6c_status w = tables_before_write(pl, st, true);
+      if (w != RAID6C_OK) return w;
       cudaFree(pl->d_prog);
       pl->d_prog = nullptr;
     }
@@ -487,6 +529,8 @@ raid6c_status upload_programs(raid6c_plan pl, const std::vector<int2>& pairs, cu
     pl->prog_cap = cap;
   }
   // pageable source: the copy is staged before this call returns, so `h` may be freed
+  raid6c_status w = tables_before_write(pl, st, false);
+  if (w != RAID6C_OK) return w;
   ZP_CUDA(cudaMemcpyAsync(pl->d_prog, h.data(), S * sizeof(zp::ExtProg), cudaMemcpyHostToDevice, st));
   return RAID6C_OK;
 }

@@ -391,3 +391,40 @@ def test_dd_solve_every_z(p):
     plan.sync()
     bad = (b.data[:, :, :nbytes] != orig[:, :, :nbytes]).nonzero()
     assert bad.numel() == 0, (p, bad[:5].tolist(), [pairs[int(i)] for i in bad[:5, 0].tolist()])
+
+
+def test_erasure_table_reuse_across_streams():
+    """A plan's device erasure table is rewritten by the next call with host pairs; when that
+    call runs on another stream (plan_set_stream), it must not overwrite the table under the
+    previous, still-running recovery (event-ordered rewrite)."""
+    p, N, nbytes = 13, 12, 4 << 20
+    big = Batch(p, N, nbytes, 48)
+    small = Batch(p, N, nbytes, 2)
+    big.fill_synthetic(seed=51, cfg=18)
+    small.fill_synthetic(seed=52, cfg=18)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    plan = R.Plan(p, N, nbytes, 0, sa)
+    plan.encode_strided(*big.args())
+    plan.set_stream(sb)
+    plan.encode_strided(*small.args())
+    plan.sync()
+    plan.set_stream(sa)
+    plan.sync()
+    ref_big, ref_small = (big.data.clone(), big.par.clone()), (small.data.clone(), small.par.clone())
+    allp = list(itertools.combinations(range(N + 2), 2))
+    pairs_big = [allp[(5 * s) % len(allp)] for s in range(big.S)]
+    pairs_small = [(0, 1), (2, 3)]
+    for s, pr in enumerate(pairs_big):
+        _poison(big, s, pr)
+    for s, pr in enumerate(pairs_small):
+        _poison(small, s, pr)
+    torch.cuda.synchronize()
+    plan.set_stream(sa)
+    plan.recover_strided(*big.args(), pairs_big)      # host pairs -> the plan's table
+    plan.set_stream(sb)
+    plan.recover_strided(*small.args(), pairs_small)  # rewrites the table on another stream
+    torch.cuda.synchronize()
+    plan.set_stream(sa)
+    plan.sync()
+    for b, (rd, rp) in ((big, ref_big), (small, ref_small)):
+        assert torch.equal(b.data, rd) and torch.equal(b.par, rp)
