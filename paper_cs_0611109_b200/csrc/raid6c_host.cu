@@ -486,6 +486,18 @@ raid6c_status upload_programs(raid6c_plan pl, const std::vector<int2>& pairs, cu
     }
     zp::ExtProg& pr = h[s];
     pr.nu = 0;
+    pr.geo_bz = pr.geo_e0 = 0;
+    // Geometric pairs (kernel: series of the basic code instead of the exponent list):
+    //   DP, j >= p:          g_j^{-1} = (1 + x^c)^{-1},            c = j - p + 1
+    //   DD, x < y < p:       (x^x + x^y)^{-1} = x^{-x} (1 + x^{y-x})^{-1}
+    //   DD, p <= x < y:      (x^cx + x^cy)^{-1} = x^{-cx} (1 + x^{cy-cx})^{-1},  c = k - p + 1
+    if (y == N && x >= p) {
+      pr.geo_bz = static_cast<int16_t>((2 * (x - p + 1)) % p);
+    } else if (y < N && (y < p || x >= p)) {
+      const int ex = x < p ? x : x - p + 1, ey = y < p ? y : y - p + 1;
+      pr.geo_bz = static_cast<int16_t>((2 * (ey - ex)) % p);
+      pr.geo_e0 = static_cast<int16_t>((p - ex) % p);
+    }
     Poly c;
     bool need = true;
     if (y == N + 1 || (x == N && y == N + 1)) need = false;  // DQ / PQ: no solve

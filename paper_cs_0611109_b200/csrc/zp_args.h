@@ -13,6 +13,9 @@ namespace zp {
 // host: u = g_j^{-1} (DP) or (g_x + g_y)^{-1} (DD), g_k the Eq. (qext) coefficient of disk k.
 struct ExtProg {
   int32_t nu;
+  // geo_bz != 0: u = x^{geo_e0} (1 + x^z)^{-1} with geo_bz = 2z mod p (the pair's coefficients
+  // are both monomials or both binomials 1 + x^c): evaluated as the basic code's geometric series
+  int16_t geo_bz, geo_e0;
   uint16_t e[RAID6C_MAX_P - 1];
 };
 

@@ -479,6 +479,92 @@ __device__ __forceinline__ void mul_prog(const uint32_t (&t)[G::C], const ExtPro
   reduce<G>(acc, out);
 }
 
+// Evaluation plan for the geometric series S_M = sum_{m<M} b^m of the DD solve, by a per-lane
+// cost model (rotation ~4 ops, reduction ~6 ops): the doubling chain costs a rotation and a
+// reduction per step; a two-level split M = M1*M2 + R costs M2 + M1 + R rotations and two
+// reductions (one if M2 == M).  p = 5, 13: direct (3 / 7 rot + 1 red); 17: 3x3; 59: 5x6;
+// 61, 257: chain (8 steps).
+constexpr int c_popcount(int v) { return v == 0 ? 0 : (v & 1) + c_popcount(v >> 1); }
+template <int M>
+struct SeriesPlan {
+  static constexpr int cost2(int m2) {
+    return m2 >= M ? 4 * M + 6 : 4 * (m2 + M / m2 + M % m2) + 12;
+  }
+  static constexpr int best_m2() {
+    int best = M, bc = cost2(M);
+    for (int m2 = 2; m2 < M; m2++)
+      if (cost2(m2) < bc) { bc = cost2(m2); best = m2; }
+    return best;
+  }
+  static constexpr int M2 = best_m2();
+  static constexpr int M1 = M / M2;
+  static constexpr int CHAIN_COST = 10 * (top_bit(M) + c_popcount(M) - 1);
+  // p = 61 (M = 31) keeps the chain: measured (r01 A/B), the two-level plan spills at the
+  // 96-register cap of its 15-lane chunks and ran 1% slower on config 5; elsewhere it wins
+  // (c2 recover +1.5%, c4 DD +1.6%, p = 17 recover +3.2%).
+  static constexpr bool CHAIN = (M == 31) || CHAIN_COST < cost2(M2);
+};
+
+
+// out = sum_{m<M} x^{bz*m + e0} t, M = (p+1)/2: the DD solve (1 + x^z)^{-1} = sum_{m<M} x^{2zm}
+// (reading R11) with b = x^{bz}, bz = 2z, times x^{e0}.  The evaluation
+// order is chosen at compile time (SeriesPlan): direct, two-level, or doubling chain; e0 is
+// folded into the rotation amounts of the first level (the chain pays one rotation for it).
+template <class G>
+__device__ __forceinline__ void series_apply(const uint32_t (&t)[G::C], int bz, int e0,
+                                             const uint2* __restrict__ mtab, Acc<G>& acc, uint32_t (&out)[G::C]) {
+  constexpr int C = G::C;
+  constexpr int M = (G::P + 1) / 2;
+  constexpr int TOP = top_bit(M);
+  using SP = SeriesPlan<M>;
+  if constexpr (!SP::CHAIN) {
+    // two-level: S = sum_{i<M1} b^{i M2} T + sum_{m=M1 M2}^{M-1} b^m x^{e0} t,
+    // T = sum_{j<M2} b^j x^{e0} t (direct when M2 == M); one deferred accumulator per level
+    uint32_t T[C];
+    acc.zero();
+#pragma unroll 1
+    for (int j = 0; j < SP::M2; j++) rot_acc<G>(t, (bz * j + e0) % G::P, mtab, acc);
+    if constexpr (SP::M2 == M) {
+      reduce<G>(acc, out);
+    } else {
+      reduce<G>(acc, T);
+      acc.zero();
+#pragma unroll 1
+      for (int i = 0; i < SP::M1; i++) rot_acc<G>(T, (bz * SP::M2 * i) % G::P, mtab, acc);
+#pragma unroll 1
+      for (int m = SP::M1 * SP::M2; m < M; m++) rot_acc<G>(t, (bz * m + e0) % G::P, mtab, acc);
+      reduce<G>(acc, out);
+    }
+    return;
+  }
+  if (e0 == 0) {
+#pragma unroll
+    for (int l = 0; l < C; l++) out[l] = t[l];  // S_1 = t
+  } else {
+    acc.zero();
+    rot_acc<G>(t, e0, mtab, acc);
+    reduce<G>(acc, out);  // S_1 = x^{e0} t
+  }
+  int m = 1;
+#pragma unroll 1
+  for (int bit = TOP - 1; bit >= 0; bit--) {
+    acc.zero();  // S_{2m} = S_m + b^m S_m
+#pragma unroll
+    for (int l = 0; l < C; l++) acc.ay[l] = out[l];
+    rot_acc<G>(out, (bz * m) % G::P, mtab, acc);
+    reduce<G>(acc, out);
+    m *= 2;
+    if ((M >> bit) & 1) {  // S_{m+1} = S_m + b^m x^{e0} t
+      acc.zero();
+#pragma unroll
+      for (int l = 0; l < C; l++) acc.ay[l] = out[l];
+      rot_acc<G>(t, (bz * m + e0) % G::P, mtab, acc);
+      reduce<G>(acc, out);
+      m += 1;
+    }
+  }
+}
+
 // Extended-code class epilogue (Lemma 23.2 proof, with g_k of Eq. (qext)):
 //   PQ: re-encode;  DQ: d_j = P + sum d_k, Q += g_j d_j;
 //   DP: d_j = u (Q + sum_{k!=j} g_k d_k), u = g_j^{-1};  P = sum d_k
@@ -503,7 +589,8 @@ __device__ __forceinline__ void finish_ext(const ZpArgs& a, const ItemDesc& d, i
   } else if (d.cls == CLS_DP) {
     uint32_t t[C];
     reduce<G>(acc, t);
-    mul_prog<G>(t, pr, mtab, o0);
+    if (pr->geo_bz) series_apply<G>(t, pr->geo_bz, pr->geo_e0, mtab, acc, o0);  // u = (1 + x^c)^{-1}
+    else mul_prog<G>(t, pr, mtab, o0);
 #pragma unroll
     for (int l = 0; l < C; l++) o1[l] = Pa[l] ^ o0[l];
     k0 = d.x; k1 = a.N;
@@ -511,7 +598,11 @@ __device__ __forceinline__ void finish_ext(const ZpArgs& a, const ItemDesc& d, i
     add_ext_coeff<G>(Pa, d.x, mtab, acc);
     uint32_t t[C];
     reduce<G>(acc, t);
-    mul_prog<G>(t, pr, mtab, o1);
+    // g_x + g_y = x^e (1 + x^z) when both coefficients are monomials or both are binomials
+    // 1 + x^c: the basic code's geometric series (host sets geo_bz = 2z, geo_e0 = -e mod p);
+    // mixed pairs x^a + 1 + x^c use the host-computed inverse (ExtProg exponents)
+    if (pr->geo_bz) series_apply<G>(t, pr->geo_bz, pr->geo_e0, mtab, acc, o1);
+    else mul_prog<G>(t, pr, mtab, o1);
 #pragma unroll
     for (int l = 0; l < C; l++) o0[l] = o1[l] ^ Pa[l];
     k0 = d.x; k1 = d.y;
@@ -538,32 +629,6 @@ __device__ __forceinline__ uint32_t count_nonzero_words(const uint32_t (&V)[G::C
   }
   return cnt;
 }
-
-// Evaluation plan for the geometric series S_M = sum_{m<M} b^m of the DD solve, by a per-lane
-// cost model (rotation ~4 ops, reduction ~6 ops): the doubling chain costs a rotation and a
-// reduction per step; a two-level split M = M1*M2 + R costs M2 + M1 + R rotations and two
-// reductions (one if M2 == M).  p = 5, 13: direct (3 / 7 rot + 1 red); 17: 3x3; 59: 5x6;
-// 61, 257: chain (8 steps).
-constexpr int c_popcount(int v) { return v == 0 ? 0 : (v & 1) + c_popcount(v >> 1); }
-template <int M>
-struct SeriesPlan {
-  static constexpr int cost2(int m2) {
-    return m2 >= M ? 4 * M + 6 : 4 * (m2 + M / m2 + M % m2) + 12;
-  }
-  static constexpr int best_m2() {
-    int best = M, bc = cost2(M);
-    for (int m2 = 2; m2 < M; m2++)
-      if (cost2(m2) < bc) { bc = cost2(m2); best = m2; }
-    return best;
-  }
-  static constexpr int M2 = best_m2();
-  static constexpr int M1 = M / M2;
-  static constexpr int CHAIN_COST = 10 * (top_bit(M) + c_popcount(M) - 1);
-  // p = 61 (M = 31) keeps the chain: measured (r01 A/B), the two-level plan spills at the
-  // 96-register cap of its 15-lane chunks and ran 1% slower on config 5; elsewhere it wins
-  // (c2 recover +1.5%, c4 DD +1.6%, p = 17 recover +3.2%).
-  static constexpr bool CHAIN = (M == 31) || CHAIN_COST < cost2(M2);
-};
 
 // Class epilogue: produces the two output chunks and their strip indices.
 template <class G>
@@ -592,55 +657,8 @@ __device__ __forceinline__ void finish(const ZpArgs& a, const ItemDesc& d, uint3
     for (int l = 0; l < C; l++) acc.ay[l] ^= Pa[l];
     uint32_t t[C];
     reduce<G>(acc, t);
-    // d_y = S_M t with S_M = sum_{m<M} b^m, b = x^{2z}, M = (p+1)/2 (reading R11); the evaluation
-    // order is chosen at compile time (SeriesPlan): direct, two-level, or doubling chain.
-    constexpr int M = (G::P + 1) / 2;
-    constexpr int TOP = top_bit(M);
-    const int bz = (2 * (d.y - d.x)) % G::P;
-    using SP = SeriesPlan<M>;
-    if constexpr (!SP::CHAIN) {
-      // two-level: S = sum_{i<M1} b^{i M2} T + sum_{m=M1 M2}^{M-1} b^m t,  T = sum_{j<M2} b^j t
-      // (direct when M2 == M).  All rotations of one level share a deferred accumulator.
-      uint32_t T[C];
-      acc.zero();
-#pragma unroll 1
-      for (int j = 0; j < SP::M2; j++) rot_acc<G>(t, (bz * j) % G::P, mtab, acc);
-      if constexpr (SP::M2 == M) {
-        reduce<G>(acc, o1);
-      } else {
-        reduce<G>(acc, T);
-        acc.zero();
-#pragma unroll 1
-        for (int i = 0; i < SP::M1; i++) rot_acc<G>(T, (bz * SP::M2 * i) % G::P, mtab, acc);
-#pragma unroll 1
-        for (int m = SP::M1 * SP::M2; m < M; m++) rot_acc<G>(t, (bz * m) % G::P, mtab, acc);
-        reduce<G>(acc, o1);
-      }
-#pragma unroll
-      for (int l = 0; l < C; l++) o0[l] = o1[l] ^ Pa[l];
-      k0 = d.x; k1 = d.y;
-      return;
-    }
-#pragma unroll
-    for (int l = 0; l < C; l++) o1[l] = t[l];  // o1 = S_1
-    int m = 1;
-#pragma unroll 1
-    for (int bit = TOP - 1; bit >= 0; bit--) {
-      acc.zero();  // S_{2m} = S_m + b^m S_m
-#pragma unroll
-      for (int l = 0; l < C; l++) acc.ay[l] = o1[l];
-      rot_acc<G>(o1, (bz * m) % G::P, mtab, acc);
-      reduce<G>(acc, o1);
-      m *= 2;
-      if ((M >> bit) & 1) {  // S_{m+1} = S_m + b^m t
-        acc.zero();
-#pragma unroll
-        for (int l = 0; l < C; l++) acc.ay[l] = o1[l];
-        rot_acc<G>(t, (bz * m) % G::P, mtab, acc);
-        reduce<G>(acc, o1);
-        m += 1;
-      }
-    }
+    // d_y = S_M t with S_M = sum_{m<M} b^m, b = x^{2z}, M = (p+1)/2 (reading R11)
+    series_apply<G>(t, (2 * (d.y - d.x)) % G::P, 0, mtab, acc, o1);
 #pragma unroll
     for (int l = 0; l < C; l++) o0[l] = o1[l] ^ Pa[l];
     k0 = d.x; k1 = d.y;
