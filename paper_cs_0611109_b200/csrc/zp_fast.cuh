@@ -57,8 +57,9 @@ constexpr int top_bit(int v) { return v <= 1 ? 0 : 1 + top_bit(v >> 1); }
 // Chunk / tile geometry of one kernel instantiation.  SMALL8_ selects, for lane-aligned small
 // words (n | 32: p = 3, 5, 17), 32-byte chunks x 256 threads = 8 KiB tiles, which divide
 // power-of-two strips exactly (no ragged tail); it is used by the light-ALU modes (encode,
-// partial: measured +6% on config 1 and +7% for p = 17), while the recovery modes keep 48-byte
-// chunks (fewer per-chunk epilogue overheads per byte: C8 measured -10% there).
+// partial: measured +6% on config 1 and +7% for p = 17) and by the NEXT-4 combine (whose word
+// ranges are whole partial tiles), while recovery keeps 48-byte chunks (fewer per-chunk epilogue
+// overheads per byte: C8 measured -10% there).
 template <int P_, bool SMALL8_ = false>
 struct Geo {
   static constexpr int P = P_;
@@ -302,7 +303,7 @@ enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3,
 constexpr int NUM_MODES = 6;
 // Geometry of mode MODE's kernel for prime P (see Geo).
 template <int P, int MODE>
-using GeoM = Geo<P, MODE == MODE_ENCODE || MODE == MODE_PARTIAL>;
+using GeoM = Geo<P, MODE == MODE_ENCODE || MODE == MODE_PARTIAL || MODE == MODE_COMBINE>;
 constexpr int K_NEW = -1;     // row index of the update's new-data buffer
 constexpr int K_PART_P = -2;  // partial-mode outputs (slots of the word-range owners)
 constexpr int K_PART_Q = -3;
