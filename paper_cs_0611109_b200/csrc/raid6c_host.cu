@@ -255,6 +255,8 @@ struct DeviceGuard {
   }
 };
 
+raid6c_status build_prog_table(raid6c_plan pl);
+
 raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, cudaStream_t stream) {
   if (!is_valid_p(p)) return RAID6C_E_INVALID_P;
   if (N < 1 || N > 2 * p - 1 || (N > p && !ext_supported_p(p))) return RAID6C_E_INVALID_N;
@@ -279,6 +281,10 @@ raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, 
   pl->stream = stream;
   pl->num_sms = prop.multiProcessorCount;
   pl->ext = N > p;
+  if (pl->ext) {
+    raid6c_status st = build_prog_table(pl);
+    if (st != RAID6C_OK) return st;
+  }
   pl->fe = zp::fast_entry(p);
   if (pl->fe && pl->ext && !pl->fe->kernel_ext[0]) pl->fe = nullptr;  // no fast extended kernels: generic
   if (pl->fe) {
@@ -434,8 +440,7 @@ raid6c_status tables_after_read(raid6c_plan pl, const zp::ZpArgs& a, cudaStream_
   const bool uses_er = pl->d_er && ((a.er >= pl->d_er && a.er < pl->d_er + pl->er_cap) ||
                                     (reinterpret_cast<const int2*>(a.upd) >= pl->d_er &&
                                      reinterpret_cast<const int2*>(a.upd) < pl->d_er + pl->er_cap));
-  const bool uses_prog = pl->d_prog && a.prog >= pl->d_prog && a.prog < pl->d_prog + pl->prog_cap;
-  if (!uses_er && !uses_prog) return RAID6C_OK;
+  if (!uses_er) return RAID6C_OK;  // (the extended code's program table is never rewritten)
   if (!pl->tables_done) ZP_CUDA(cudaEventCreateWithFlags(&pl->tables_done, cudaEventDisableTiming));
   ZP_CUDA(cudaEventRecord(pl->tables_done, st));
   pl->tables_pending = true;
@@ -471,79 +476,67 @@ raid6c_status upload_erasures(raid6c_plan pl, const raid6c_erasure* er, int coun
   return RAID6C_OK;
 }
 
-// Extended code: per-stripe multiplier u for the DP / DD solves (ExtProg), uploaded into the
-// plan's device buffer.  pairs: canonical (x < y) per stripe.
-raid6c_status upload_programs(raid6c_plan pl, const std::vector<int2>& pairs, cudaStream_t st) {
-  const int p = pl->p, N = pl->N, S = static_cast<int>(pairs.size());
-  std::vector<zp::ExtProg> h(S);
-  std::map<std::pair<int, int>, int> memo;
-  for (int s = 0; s < S; s++) {
-    const int x = pairs[s].x, y = pairs[s].y;
-    auto it = memo.find({x, y});
-    if (it != memo.end()) {
-      h[s] = h[it->second];
-      continue;
-    }
-    zp::ExtProg& pr = h[s];
-    pr.nu = 0;
-    pr.geo_bz = pr.geo_e0 = 0;
-    // Geometric pairs (kernel: series of the basic code instead of the exponent list):
-    //   DP, j >= p:          g_j^{-1} = (1 + x^c)^{-1},            c = j - p + 1
-    //   DD, x < y < p:       (x^x + x^y)^{-1} = x^{-x} (1 + x^{y-x})^{-1}
-    //   DD, p <= x < y:      (x^cx + x^cy)^{-1} = x^{-cx} (1 + x^{cy-cx})^{-1},  c = k - p + 1
-    if (y == N && x >= p) {
-      pr.geo_bz = static_cast<int16_t>((2 * (x - p + 1)) % p);
-    } else if (y < N && (y < p || x >= p)) {
-      const int ex = x < p ? x : x - p + 1, ey = y < p ? y : y - p + 1;
-      pr.geo_bz = static_cast<int16_t>((2 * (ey - ex)) % p);
-      pr.geo_e0 = static_cast<int16_t>((p - ex) % p);
-    }
-    Poly c;
-    bool need = true;
-    if (y == N + 1 || (x == N && y == N + 1)) need = false;  // DQ / PQ: no solve
-    else if (y == N) c = ext_coeff(p, x);                     // DP: u = g_x^{-1}
-    else {                                                    // DD: u = (g_x + g_y)^{-1}
-      c = ext_coeff(p, x);
-      Poly cy = ext_coeff(p, y);
-      for (int i = 0; i < Poly::L; i++) c.w[i] ^= cy.w[i];
-    }
-    if (need) {
-      Poly u;
-      if (!ring_inverse(c, p, u)) {
-        g_last_err = "extended code: coefficient not invertible";
-        return RAID6C_E_INVALID_N;
-      }
-      for (int i = 0; i < p - 1; i++)
-        if (u.bit(i)) pr.e[pr.nu++] = static_cast<uint16_t>(i);
-      // u and u + (1 + x + ... + x^{p-1}) are the same element of R_p (the p-th roots of unity
-      // sum to zero, Lemma 24.2), and the kernel multiplies in R' with
-      // deferred reduction: take whichever has fewer terms (the complement includes x^{p-1}).
-      if (2 * pr.nu > p) {
-        int k = 0;
-        for (int i = 0; i < p; i++)
-          if (i == p - 1 || !u.bit(i)) pr.e[k++] = static_cast<uint16_t>(i);
-        pr.nu = k;
-      }
-    }
-    memo[{x, y}] = s;
+// Extended code: the multiplier u of the DP / DD solve of pair (x, y), x < y (ExtProg).
+raid6c_status make_prog(int p, int N, int x, int y, zp::ExtProg& pr) {
+  std::memset(&pr, 0, sizeof(pr));
+  // Geometric pairs (kernel: series of the basic code instead of the exponent list):
+  //   DP, j >= p:          g_j^{-1} = (1 + x^c)^{-1},            c = j - p + 1
+  //   DD, x < y < p:       (x^x + x^y)^{-1} = x^{-x} (1 + x^{y-x})^{-1}
+  //   DD, p <= x < y:      (x^cx + x^cy)^{-1} = x^{-cx} (1 + x^{cy-cx})^{-1},  c = k - p + 1
+  if (y == N && x >= p) {
+    pr.geo_bz = static_cast<int16_t>((2 * (x - p + 1)) % p);
+    return RAID6C_OK;
   }
-  if (static_cast<size_t>(S) > pl->prog_cap) {
-    DeviceGuard g(pl->device);
-    if (pl->d_prog) {
-      ZP_CUDA(cudaStreamSynchronize(st));
-      raid6c_status w = tables_before_write(pl, st, true);
-      if (w != RAID6C_OK) return w;
-      cudaFree(pl->d_prog);
-      pl->d_prog = nullptr;
-    }
-    const size_t cap = std::max<size_t>(64, static_cast<size_t>(S));
-    ZP_CUDA(cudaMalloc(&pl->d_prog, cap * sizeof(zp::ExtProg)));
-    pl->prog_cap = cap;
+  if (y < N && (y < p || x >= p)) {
+    const int ex = x < p ? x : x - p + 1, ey = y < p ? y : y - p + 1;
+    pr.geo_bz = static_cast<int16_t>((2 * (ey - ex)) % p);
+    pr.geo_e0 = static_cast<int16_t>((p - ex) % p);
+    return RAID6C_OK;
   }
-  // pageable source: the copy is staged before this call returns, so `h` may be freed
-  raid6c_status w = tables_before_write(pl, st, false);
-  if (w != RAID6C_OK) return w;
-  ZP_CUDA(cudaMemcpyAsync(pl->d_prog, h.data(), S * sizeof(zp::ExtProg), cudaMemcpyHostToDevice, st));
+  Poly c;
+  if (y == N + 1) return RAID6C_OK;  // DQ / PQ: no solve
+  if (y == N) {                      // DP, j < p: u = g_j^{-1} = x^{p-j}
+    c = ext_coeff(p, x);
+  } else {                           // DD, mixed pair: u = (x^a + 1 + x^c)^{-1}
+    c = ext_coeff(p, x);
+    Poly cy = ext_coeff(p, y);
+    for (int i = 0; i < Poly::L; i++) c.w[i] ^= cy.w[i];
+  }
+  Poly u;
+  if (!ring_inverse(c, p, u)) {
+    g_last_err = "extended code: coefficient not invertible";
+    return RAID6C_E_INVALID_N;
+  }
+  for (int i = 0; i < p - 1; i++)
+    if (u.bit(i)) pr.e[pr.nu++] = static_cast<uint16_t>(i);
+  // u and u + (1 + x + ... + x^{p-1}) are the same element of R_p (the p-th roots of unity
+  // sum to zero, Lemma 24.2), and the kernel multiplies in R' with
+  // deferred reduction: take whichever has fewer terms (the complement includes x^{p-1}).
+  if (2 * pr.nu > p) {
+    int k = 0;
+    for (int i = 0; i < p; i++)
+      if (i == p - 1 || !u.bit(i)) pr.e[k++] = static_cast<uint16_t>(i);
+    pr.nu = k;
+  }
+  return RAID6C_OK;
+}
+
+// Extended-code plans: the multipliers of every pair, indexed by zp::pair_index, built and
+// uploaded once at plan creation -- so a recovery whose per-stripe pairs live on the device
+// needs no host round trip.
+raid6c_status build_prog_table(raid6c_plan pl) {
+  const int p = pl->p, N = pl->N, K = N + 2;
+  const size_t n = static_cast<size_t>(K) * (K - 1) / 2;
+  std::vector<zp::ExtProg> h(n);
+  for (int x = 0; x < K; x++)
+    for (int y = x + 1; y < K; y++) {
+      raid6c_status st = make_prog(p, N, x, y, h[zp::pair_index(x, y, N)]);
+      if (st != RAID6C_OK) return st;
+    }
+  DeviceGuard g(pl->device);
+  ZP_CUDA(cudaMalloc(&pl->d_prog, n * sizeof(zp::ExtProg)));
+  pl->prog_cap = n;
+  ZP_CUDA(cudaMemcpy(pl->d_prog, h.data(), n * sizeof(zp::ExtProg), cudaMemcpyHostToDevice));
   return RAID6C_OK;
 }
 
@@ -554,24 +547,7 @@ raid6c_status set_erasures(raid6c_plan plan, zp::ZpArgs& a, const raid6c_erasure
                            int erasures_on_device, int num_stripes, bool with_programs) {
   raid6c_status st = RAID6C_OK;
   if (num_erasures != 1 && num_erasures != num_stripes) return RAID6C_E_SIZE;
-  if (plan->ext && with_programs) {  // extended code: per-stripe multipliers are built on the host from the pairs
-    std::vector<raid6c_erasure> hp(num_erasures);
-    if (erasures_on_device) {
-      ZP_CUDA(cudaMemcpy(hp.data(), erasures, num_erasures * sizeof(raid6c_erasure), cudaMemcpyDeviceToHost));
-    } else {
-      std::copy(erasures, erasures + num_erasures, hp.begin());
-    }
-    std::vector<int2> pairs(num_erasures);
-    for (int s2 = 0; s2 < num_erasures; s2++) {
-      st = check_erasure(plan->N, hp[s2].lost_i, hp[s2].lost_j);
-      if (st != RAID6C_OK) return st;
-      pairs[s2] = make_int2(std::min(hp[s2].lost_i, hp[s2].lost_j), std::max(hp[s2].lost_i, hp[s2].lost_j));
-    }
-    st = upload_programs(plan, pairs, plan->stream);
-    if (st != RAID6C_OK) return st;
-    a.prog = plan->d_prog;
-    a.prog_stride = num_erasures == 1 ? 0 : 1;
-  }
+  if (plan->ext && with_programs) a.prog = plan->d_prog;  // per-pair table (build_prog_table)
   if (erasures_on_device) {
     a.er = reinterpret_cast<const int2*>(erasures);
     a.er_stride = num_erasures == 1 ? 0 : 1;
@@ -614,6 +590,7 @@ raid6c_status cached_plan(int p, int N, size_t bytes, raid6c_plan* out) {
   raid6c_plan pl = new raid6c_plan_s();
   raid6c_status st = plan_init(pl, p, N, bytes, dev, nullptr);
   if (st != RAID6C_OK) {
+    plan_release(pl);
     delete pl;
     return st;
   }
@@ -706,10 +683,6 @@ raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_
     for (int s = 0; s < num_stripes; s++) ev[s] = {pairs[s].x, pairs[s].y};
     st = upload_erasures(pl, ev.data(), num_stripes, s_k);
     if (st != RAID6C_OK) return st;
-    if (pl->ext) {
-      st = upload_programs(pl, pairs, s_k);
-      if (st != RAID6C_OK) return st;
-    }
   }
   // order after anything already queued on the plan stream
   ZP_CUDA(cudaEventRecord(pl->ev_out[0], pl->stream));
@@ -771,10 +744,7 @@ raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_
     if (recover) {
       a.er = pl->d_er + s0;
       a.er_stride = 1;
-      if (pl->ext) {
-        a.prog = pl->d_prog + s0;
-        a.prog_stride = 1;
-      }
+      if (pl->ext) a.prog = pl->d_prog;
     }
     st = launch(pl, a, recover ? zp::KMODE_RECOVER : zp::KMODE_ENCODE, s_k);
     if (st != RAID6C_OK) return st;
@@ -853,6 +823,7 @@ raid6c_status raid6c_plan_create(raid6c_plan* out, int p, int N, size_t bytes, i
   raid6c_plan pl = new raid6c_plan_s();
   raid6c_status st = plan_init(pl, p, N, bytes, device, static_cast<cudaStream_t>(stream));
   if (st != RAID6C_OK) {
+    plan_release(pl);  // (buffers allocated before the failure, e.g. the program table)
     delete pl;
     return st;
   }
@@ -935,12 +906,7 @@ raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* cons
   a.ei = std::min(lost_i, lost_j);
   a.ej = std::max(lost_i, lost_j);
   std::unique_lock<std::mutex> lk(pl->mu);
-  if (pl->ext) {
-    st = upload_programs(pl, {make_int2(a.ei, a.ej)}, nullptr);
-    if (st != RAID6C_OK) return st;
-    a.prog = pl->d_prog;
-    a.prog_stride = 0;
-  }
+  if (pl->ext) a.prog = pl->d_prog;
   st = launch(pl, a, zp::KMODE_RECOVER, nullptr);
   if (st != RAID6C_OK) return st;
   ZP_CUDA(cudaStreamSynchronize(nullptr));

@@ -47,9 +47,9 @@ struct ZpArgs {
   const uint8_t* nbase;
   uint64_t new_stride;
   uint32_t* counts;
-  // NEXT-2: multiplier programs for the extended code (prog[s * prog_stride]); N > p only.
+  // NEXT-2: multiplier programs for the extended code, one per erasure pair
+  // (prog[pair_index(x, y, N)]); N > p only.
   const ExtProg* prog;
-  int prog_stride;
   // NEXT-4 (cross-GPU stripe layout, include/raid6c.h).  partial: rows = the surviving strips
   // with global index in [k_lo, k_hi); word range g of its two outputs goes to
   // part_p[g] / part_q[g] + s*part_stride + (off - g*range_bytes).
@@ -83,6 +83,12 @@ struct FastEntry {
 };
 
 const FastEntry* fast_entry(int p);  // nullptr if p has no fast path
+
+// Index of the canonical pair (x < y) among the C(N+2, 2) pairs of strip indices, row-major.
+__host__ __device__ inline int pair_index(int x, int y, int N) {
+  const int K = N + 2;
+  return x * (2 * K - x - 1) / 2 + (y - x - 1);
+}
 
 // Generic (runtime-p) kernels, any odd prime <= 257.
 enum : int { KMODE_ENCODE = 0, KMODE_RECOVER = 1, KMODE_SCRUB = 2, KMODE_UPDATE = 3, KMODE_PARTIAL = 4,

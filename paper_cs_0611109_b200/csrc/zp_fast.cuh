@@ -575,7 +575,7 @@ __device__ __forceinline__ void finish_ext(const ZpArgs& a, const ItemDesc& d, i
                                            const uint2* __restrict__ mtab, uint32_t (&o0)[G::C],
                                            uint32_t (&o1)[G::C], int& k0, int& k1) {
   constexpr int C = G::C;
-  const ExtProg* pr = a.prog + static_cast<int64_t>(s) * a.prog_stride;
+  const ExtProg* pr = a.prog + pair_index(d.x, d.y, a.N);
   if (d.cls == CLS_PQ) {
 #pragma unroll
     for (int l = 0; l < C; l++) o0[l] = Pa[l];

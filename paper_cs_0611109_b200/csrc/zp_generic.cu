@@ -111,10 +111,15 @@ __device__ void add_coeff(Word& acc, const Word& v, int k, int p) {
   }
 }
 
-// out = u * t, u = sum_i x^{e_i} from the stripe's ExtProg.
+// out = u * t for the pair's ExtProg: u = sum_i x^{e_i}, or, for a geometric pair,
+// u = x^{e0} sum_{m<(p+1)/2} x^{bz m} (= x^{e0} (1 + x^{bz/2})^{-1}, reading R11).
 __device__ void mul_prog(const Word& t, const ExtProg* pr, int p, Word& out) {
   wzero(out);
-  for (int i = 0; i < pr->nu; i++) rot_acc(out, t, pr->e[i], p);
+  if (pr->geo_bz) {
+    for (int m = 0; m < (p + 1) / 2; m++) rot_acc(out, t, (pr->geo_bz * m + pr->geo_e0) % p, p);
+  } else {
+    for (int i = 0; i < pr->nu; i++) rot_acc(out, t, pr->e[i], p);
+  }
   reduce(out, p);
 }
 
@@ -216,7 +221,7 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
           }
         }
       }
-      const ExtProg* pr = ext ? a.prog + static_cast<int64_t>(s) * a.prog_stride : nullptr;
+      const ExtProg* pr = ext ? a.prog + pair_index(d.x, d.y, a.N) : nullptr;
       if (mode == KMODE_PARTIAL) {  // unsolved partial syndromes (NEXT-4)
         o[0] = Pa;
         reduce(acc, p);
