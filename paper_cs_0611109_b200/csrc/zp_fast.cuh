@@ -74,7 +74,6 @@ struct Geo {
   static constexpr int THREADS = SMALL8 ? 256 : (C >= 24 ? 128 : ((32 % n == 0) ? 224 : 256));
   static constexpr int TB = THREADS * CB;            // TMA row (tile) bytes
   static constexpr int MTAB = (n + 1) * LAMBDA;      // mask table entries (uint2)
-  static constexpr int SMEM_TARGET = 112 * 1024;     // 2 CTAs per SM
   static_assert(LAMBDA <= 32, "fast path needs a period of at most 32 lanes");
   static_assert(TB % 16 == 0, "TMA rows must be multiples of 16 bytes");
 };
@@ -689,11 +688,23 @@ __device__ __forceinline__ void build_mtab(uint2* mtab) {
 }
 
 // Shared-memory layout per (p, mode): STAGES TMA rows, NOUT output rows, mask table, barriers.
+// CTAs per SM that the kernel of (P, MODE) is built for: the register cap of
+// __launch_bounds__ and the shared-memory budget per CTA (112 KB for 2, 72 KB for 3).  Measured
+// (r01 A/B): encode of 6-, 12- and 256-bit words gains from a third CTA (p = 13: 0.97 -> 1.06 of
+// the copy rate, p = 7: 0.98 -> 1.08, p = 257: 1.02 -> 1.05; 72 registers), and the NEXT-4
+// partial with it (+0-4%), while every recovery mode and the other primes' encode lose with it
+// (spills at 128 / 72 registers for p = 59 / 61, a 63-register cap for the 8 KiB-tile primes).
+template <int P, int MODE>
+__host__ __device__ constexpr int min_blocks() {
+  return ((P == 7 || P == 13 || P == 257) && (MODE == MODE_ENCODE || MODE == MODE_PARTIAL)) ? 3 : 2;
+}
+
 template <int P, int MODE>
 struct Layout {
   using G = GeoM<P, MODE>;
   static constexpr int NOUT = num_outputs<MODE>();
-  static constexpr int STAGES_RAW = (G::SMEM_TARGET - NOUT * G::TB - G::MTAB * 8 - 256) / G::TB;
+  static constexpr int SMEM_TARGET = min_blocks<P, MODE>() == 3 ? 72 * 1024 : 112 * 1024;
+  static constexpr int STAGES_RAW = (SMEM_TARGET - NOUT * G::TB - G::MTAB * 8 - 256) / G::TB;
   static constexpr int STAGES = STAGES_RAW < 3 ? 3 : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
   static constexpr size_t SMEM = (size_t)(STAGES + NOUT) * G::TB + (size_t)G::MTAB * 8 + 2 * STAGES * 8;
 };
@@ -737,7 +748,7 @@ __device__ __forceinline__ void epilogue(const ZpArgs& a, const ItemDesc& d, int
 }
 
 template <int P, int MODE, bool EXT = false>
-__global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, 2) zp_kernel(const __grid_constant__ ZpArgs a) {
+__global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (min_blocks<P, MODE>())) zp_kernel(const __grid_constant__ ZpArgs a) {
   using G = GeoM<P, MODE>;
   using LY = Layout<P, MODE>;
   constexpr int C = G::C, CB = G::CB, TB = G::TB, NT = G::THREADS, ST = LY::STAGES, NOUT = LY::NOUT;
