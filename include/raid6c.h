@@ -211,7 +211,7 @@ raid6c_status raid6c_rs_recover_strided(int N, size_t bytes, uint8_t *data, size
  *      into part_p[g] / part_q[g] -- a slot owned by rank g, local or a peer pointer
  *      (NVLink stores, overlapped with the fold tile by tile).
  *   2. raid6c_combine_strided: rank g XORs the num_sources partial slots of its word range
- *      (local memory, or peer pointers to pull from) and applies the class solve of
+ *      (in the owner's memory; peer pointers are accepted too) and applies the class solve of
  *      Lemma 23.2 / Sec. 4.6 in the same kernel, writing the
  *      rebuilt strips (or P and Q for an encode) straight to their owners (peer pointers).
  *
