@@ -80,3 +80,18 @@ def test_build_and_shard_import_without_library():
             "    assert 'no CPU fallback' in str(e); print('ok')\n")
     r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True)
     assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr
+
+
+def _build_c_example(out):
+    cmd = ["gcc", "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+           os.path.join(ROOT, "examples", "c_api_roundtrip.c"), "-L", os.path.dirname(R.LIB_PATH), "-lraid6c",
+           "-L", "/usr/local/cuda/lib64", "-lcudart", f"-Wl,-rpath,{os.path.dirname(R.LIB_PATH)}", "-o", out]
+    return subprocess.run(cmd, capture_output=True, text=True)
+
+
+def test_c_example_compiles_and_links(tmp_path):
+    """The boundary is a plain C ABI: a C program includes raid6c.h and links libraid6c.so."""
+    if os.path.basename(R.LIB_PATH) != "libraid6c.so":
+        pytest.skip("variant library")
+    r = _build_c_example(str(tmp_path / "c_api_roundtrip"))
+    assert r.returncode == 0, r.stderr

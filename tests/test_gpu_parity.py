@@ -428,3 +428,17 @@ def test_erasure_table_reuse_across_streams():
     plan.sync()
     for b, (rd, rp) in ((big, ref_big), (small, ref_small)):
         assert torch.equal(b.data, rd) and torch.equal(b.par, rp)
+
+
+@pytest.mark.parametrize("args", [("13", "12", "1000003", "8"), ("59", "58", "300001", "4"), ("11", "10", "5000", "4"),
+                                  ("13", "25", "100000", "4"), ("5", "1", "777", "4")])
+def test_c_example_roundtrip(tmp_path, args):
+    """examples/c_api_roundtrip.c: encode + recovery of every class through the C ABI from C."""
+    import subprocess
+    from tests.test_abi import _build_c_example
+    exe = str(tmp_path / "c_api_roundtrip")
+    r = _build_c_example(exe)
+    assert r.returncode == 0, r.stderr
+    r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert " 0 strips differ" in r.stdout
