@@ -977,6 +977,9 @@ def main():
     if args.warmup < 3 and args.impl == "ours":
         print("note: warm-up raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3
+    if args.gpus > 1 and _env_rank()[1] == 1:
+        print(f"note: --gpus {args.gpus} without a torchrun launch runs one rank (launch with "
+              f"python -m torch.distributed.run --nproc-per-node {args.gpus} ...)", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     elif args.op != "step":
