@@ -34,6 +34,11 @@ __device__ __forceinline__ void op(uint32_t& a, uint32_t b, uint32_t c) {
   if constexpr (OP == 1) asm volatile("shf.l.wrap.b32 %0, %0, %1, %2;" : "+r"(a) : "r"(b), "r"(c));
   if constexpr (OP == 2) asm volatile("add.u32 %0, %0, %1;" : "+r"(a) : "r"(b));
   if constexpr (OP == 3) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a) : "r"(b), "r"(c));
+  if constexpr (OP == 4) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a) : "r"(b), "r"(c));
+  if constexpr (OP == 5) {  // mixed stream: 1 funnel shift (ALU) + 1 multiply-add (FMA) per op pair
+    asm volatile("shf.l.wrap.b32 %0, %0, %1, %2;" : "+r"(a) : "r"(b), "r"(c));
+    asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a) : "r"(b), "r"(c));
+  }
 }
 template <int OP>
 __global__ void alu_kernel(uint32_t* out, int iters, unsigned long long* cyc) {
@@ -126,9 +131,10 @@ int main() {
   CK(cudaMalloc(&out, 1 << 20));
   CK(cudaMalloc(&cyc, 8));
   printf("{\"sms\": %d, \"attr_clock_mhz\": %.0f,\n \"int_ops_per_clk_per_sm\": {", sms, clk_khz / 1e3);
-  const char* names[4] = {"LOP3", "SHF.L.W", "IADD3 (2 PTX adds fused per op: counts PTX adds)", "IMAD"};
+  const char* names[6] = {"LOP3", "SHF.L.W", "IADD3 (2 PTX adds fused per op: counts PTX adds)", "IMAD", "IMAD.HI",
+                          "SHF+IMAD mixed (counts both)"};
   const int blocks = sms * 2, threads = 512, iters = 4096;  // 32 warps per SM
-  for (int o = 0; o < 4; o++) {
+  for (int o = 0; o < 6; o++) {
     float best = 0;
     for (int rep = 0; rep < 3; rep++) {
       CK(cudaMemset(cyc, 0, 8));
@@ -136,10 +142,12 @@ int main() {
       if (o == 1) alu_kernel<1><<<blocks, threads>>>(out, iters, cyc);
       if (o == 2) alu_kernel<2><<<blocks, threads>>>(out, iters, cyc);
       if (o == 3) alu_kernel<3><<<blocks, threads>>>(out, iters, cyc);
+      if (o == 4) alu_kernel<4><<<blocks, threads>>>(out, iters, cyc);
+      if (o == 5) alu_kernel<5><<<blocks, threads>>>(out, iters, cyc);
       CK(cudaDeviceSynchronize());
       unsigned long long c = 0;
       CK(cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost));
-      const double ops_per_sm = 2.0 * threads * iters * 4.0 * 8.0;  // 2 blocks per SM
+      const double ops_per_sm = 2.0 * threads * iters * 4.0 * 8.0 * (o == 5 ? 2 : 1);  // 2 blocks per SM
       const float v = static_cast<float>(ops_per_sm / static_cast<double>(c));
       if (v > best) best = v;
     }
