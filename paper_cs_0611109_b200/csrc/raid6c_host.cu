@@ -23,6 +23,11 @@ namespace zp {
 const FastEntry* fast_entry_3();
 const FastEntry* fast_entry_5();
 const FastEntry* fast_entry_7();
+const FastEntry* fast_entry_11();
+const FastEntry* fast_entry_19();
+const FastEntry* fast_entry_29();
+const FastEntry* fast_entry_37();
+const FastEntry* fast_entry_53();
 const FastEntry* fast_entry_13();
 const FastEntry* fast_entry_17();
 const FastEntry* fast_entry_59();
@@ -34,6 +39,11 @@ const FastEntry* fast_entry(int p) {
     case 3: return fast_entry_3();
     case 5: return fast_entry_5();
     case 7: return fast_entry_7();
+    case 11: return fast_entry_11();
+    case 19: return fast_entry_19();
+    case 29: return fast_entry_29();
+    case 37: return fast_entry_37();
+    case 53: return fast_entry_53();
     case 13: return fast_entry_13();
     case 17: return fast_entry_17();
     case 59: return fast_entry_59();

@@ -18,7 +18,7 @@ from tests.gpu_util import Batch  # noqa: E402
 
 PRIMES = [p for p in range(3, 258) if all(p % q for q in range(2, int(p ** 0.5) + 1))]
 
-FAST = [3, 5, 7, 13, 17, 59, 61, 257]
+FAST = [3, 5, 7, 11, 13, 17, 19, 29, 37, 53, 59, 61, 257]
 
 
 def _case(seed):

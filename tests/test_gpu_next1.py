@@ -18,7 +18,7 @@ from tests.gpu_util import Batch  # noqa: E402
 
 CASES = [(13, 12, 3 * 12288 + 777, 3, 0), (5, 4, 65536, 3, 0), (59, 58, 2 * 14848 + 50, 2, 0),
          (61, 60, 2 * 15360 + 9, 2, 0), (257, 64, 2 * 8192 + 33, 2, 0), (17, 16, 12000, 2, 0),
-         (11, 10, 2000, 2, 0), (13, 12, 5000, 2, 3), (3, 3, 1000, 2, 0), (7, 7, 777, 3, 1)]
+         (11, 10, 2000, 2, 0), (23, 22, 2000, 2, 0), (13, 12, 5000, 2, 3), (3, 3, 1000, 2, 0), (7, 7, 777, 3, 1)]
 
 
 def _np(t):

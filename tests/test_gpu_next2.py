@@ -17,10 +17,10 @@ import synthetic  # noqa: E402
 from paper_cs_0611109_b200 import raid6c as R  # noqa: E402
 from tests.gpu_util import Batch  # noqa: E402
 
-# (p, N, bytes, stripes); fast-path primes and generic ones (11, 19)
+# (p, N, bytes, stripes); fast-path primes and generic ones (23, 43)
 CASES = [(5, 9, 3 * 10752 + 517, 2), (13, 25, 2 * 12288 + 99, 2), (13, 17, 5000, 2), (17, 33, 11000, 2),
          (59, 90, 14848 + 333, 2), (61, 121, 15360 + 17, 2), (257, 300, 8192 + 64, 1), (11, 21, 3000, 2),
-         (19, 37, 1500, 2)]
+         (19, 37, 1500, 2), (23, 45, 1500, 2), (43, 60, 1200, 2)]
 
 
 def _np(t):

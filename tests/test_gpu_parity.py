@@ -21,8 +21,8 @@ import synthetic  # noqa: E402
 from paper_cs_0611109_b200 import raid6c as R  # noqa: E402
 from tests.gpu_util import Batch, segment_bounds  # noqa: E402
 
-FAST = [3, 5, 7, 13, 17, 59, 61, 257]
-GENERIC = [11, 19, 23, 29, 31, 37, 97]
+FAST = [3, 5, 7, 11, 13, 17, 19, 29, 37, 53, 59, 61, 257]
+GENERIC = [23, 31, 41, 43, 47, 67, 97, 127]
 
 
 def _poison(b, s, ks):
@@ -50,6 +50,7 @@ def test_fill_matches_numpy_generator():
 # ------------------------------------------------------------------ north-star single-stripe API
 @pytest.mark.parametrize("p", FAST + GENERIC)
 def test_encode_single_matches_oracle(p):
+    assert R.has_fast_path(p) == (p in FAST)
     rng = np.random.default_rng(p)
     for N, nbytes in [(1, 1), (min(p, 3), 37), (p - 1, 5000), (p, 1024 + 7)]:
         if p == 257 and N > 70:

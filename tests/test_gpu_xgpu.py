@@ -31,7 +31,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 CASES = [(13, 12, 3 * 12288 + 1001, 3, 4), (13, 12, 3 * 12288 + 1001, 3, 1), (5, 4, 4 * 10752 + 77, 3, 3),
          (59, 58, 2 * 14848 + 333, 2, 8), (61, 60, 2 * 15360 + 17, 2, 5), (257, 64, 3 * 4096 + 64, 2, 8),
          (17, 16, 2 * 10752 + 9, 2, 2), (3, 2, 5000, 3, 4), (7, 6, 4000, 2, 3), (11, 10, 3000, 2, 3),
-         (19, 18, 2500, 2, 4), (13, 25, 2 * 12288 + 99, 2, 4), (59, 90, 14848 + 333, 1, 6)]
+         (19, 18, 2500, 2, 4), (13, 25, 2 * 12288 + 99, 2, 4), (59, 90, 14848 + 333, 1, 6),
+         (23, 22, 3000, 2, 3), (67, 40, 2000, 2, 4), (43, 60, 1500, 1, 5)]
 
 
 def _np(t):
@@ -86,7 +87,7 @@ def test_xgpu_encode_and_recover(p, N, nbytes, S, G):
                 assert np.array_equal(_np(b.strip(s, k)), refs[s][k]), (p, N, G, s, (x, y), k)
 
 
-@pytest.mark.parametrize("p,N,G", [(13, 12, 4), (59, 58, 3), (11, 10, 2)])
+@pytest.mark.parametrize("p,N,G", [(13, 12, 4), (59, 58, 3), (11, 10, 2), (23, 22, 3)])
 def test_xgpu_partials_are_oracle_subset_parity(p, N, G):
     """Encode partial of rank r = the oracle parity of the stripe with every strip outside the
     rank's block zeroed (linearity of Eq. (znparity)); unaligned slots take the direct path."""
