@@ -66,7 +66,10 @@ struct Geo {
   static constexpr int n = P - 1;
   static constexpr int LAMBDA = n / cgcd(n, 32);  // 32-bit lanes per period lcm(n,32)
   static constexpr bool SMALL8 = SMALL8_ && (32 % n == 0);
-  static constexpr int C = SMALL8 ? 8 : (LAMBDA < 12 ? LAMBDA * (12 / LAMBDA) : LAMBDA);  // lanes per chunk
+  // lanes per chunk: whole periods, at least 12 lanes (48 B) so that the per-chunk epilogue
+  // (reductions, the DD series) is amortised; measured for LAMBDA = 5, 7, 9 (p = 11, 29, 19/37):
+  // 15 / 14 / 18 lanes recover at 0.92-1.01 of the copy rate vs 0.73-0.89 with 10 / 7 / 9
+  static constexpr int C = SMALL8 ? 8 : (LAMBDA < 12 ? LAMBDA * ((12 + LAMBDA - 1) / LAMBDA) : LAMBDA);
   static constexpr int CB = 4 * C;                   // chunk bytes
   static constexpr int QMAX = n >> 5;                // max whole-lane shift
   // consumer threads per CTA; 224 for lane-aligned small words (n | 32) with 48-byte chunks so
