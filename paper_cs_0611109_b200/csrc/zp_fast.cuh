@@ -60,7 +60,7 @@ constexpr int top_bit(int v) { return v <= 1 ? 0 : 1 + top_bit(v >> 1); }
 // partial: measured +6% on config 1 and +7% for p = 17) and by the NEXT-4 combine (whose word
 // ranges are whole partial tiles), while recovery keeps 48-byte chunks (fewer per-chunk epilogue
 // overheads per byte: C8 measured -10% there).
-template <int P_, bool SMALL8_ = false>
+template <int P_, bool SMALL8_ = false, int MINLANES_ = 12>
 struct Geo {
   static constexpr int P = P_;
   static constexpr int n = P - 1;
@@ -69,7 +69,7 @@ struct Geo {
   // lanes per chunk: whole periods, at least 12 lanes (48 B) so that the per-chunk epilogue
   // (reductions, the DD series) is amortised; measured for LAMBDA = 5, 7, 9 (p = 11, 29, 19/37):
   // 15 / 14 / 18 lanes recover at 0.92-1.01 of the copy rate vs 0.73-0.89 with 10 / 7 / 9
-  static constexpr int C = SMALL8 ? 8 : (LAMBDA < 12 ? LAMBDA * ((12 + LAMBDA - 1) / LAMBDA) : LAMBDA);
+  static constexpr int C = SMALL8 ? 8 : (LAMBDA < MINLANES_ ? LAMBDA * ((MINLANES_ + LAMBDA - 1) / LAMBDA) : LAMBDA);
   static constexpr int CB = 4 * C;                   // chunk bytes
   static constexpr int QMAX = n >> 5;                // max whole-lane shift
   // consumer threads per CTA; 224 for lane-aligned small words (n | 32) with 48-byte chunks so
@@ -304,8 +304,17 @@ enum : int { CLS_PQ = 0, CLS_DQ = 1, CLS_DP = 2, CLS_DD = 3, CLS_SCRUB = 4, CLS_
 enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3, MODE_PARTIAL = 4, MODE_COMBINE = 5 };
 constexpr int NUM_MODES = 6;
 // Geometry of mode MODE's kernel for prime P (see Geo).
+// Recovery chunks of at least 15 lanes for p = 7, 13, 17 (measured r01: c2 recovery 0.96 -> 1.01
+// of the copy rate, p = 17 0.93 -> 0.98, p = 7 1.02 -> 1.05); not for p = 5 (config 1's 64 KiB
+// strips would get a 13 KiB tile with a long ragged tail: 0.91 -> 0.66) nor p = 29 (21 lanes
+// spill: 1.02 -> 0.83).
+template <int P>
+__host__ __device__ constexpr int recover_min_lanes() {
+  return (P == 7 || P == 13 || P == 17) ? 15 : 12;
+}
 template <int P, int MODE>
-using GeoM = Geo<P, MODE == MODE_ENCODE || MODE == MODE_PARTIAL || MODE == MODE_COMBINE>;
+using GeoM = Geo<P, MODE == MODE_ENCODE || MODE == MODE_PARTIAL || MODE == MODE_COMBINE,
+                 MODE == MODE_RECOVER ? recover_min_lanes<P>() : 12>;
 constexpr int K_NEW = -1;     // row index of the update's new-data buffer
 constexpr int K_PART_P = -2;  // partial-mode outputs (slots of the word-range owners)
 constexpr int K_PART_Q = -3;
