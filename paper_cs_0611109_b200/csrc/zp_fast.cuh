@@ -69,7 +69,10 @@ struct Geo {
   // lanes per chunk: whole periods, at least 12 lanes (48 B) so that the per-chunk epilogue
   // (reductions, the DD series) is amortised; measured for LAMBDA = 5, 7, 9 (p = 11, 29, 19/37):
   // 15 / 14 / 18 lanes recover at 0.92-1.01 of the copy rate vs 0.73-0.89 with 10 / 7 / 9
-  static constexpr int C = SMALL8 ? 8 : (LAMBDA < MINLANES_ ? LAMBDA * ((MINLANES_ + LAMBDA - 1) / LAMBDA) : LAMBDA);
+  // (words that are whole lanes, n = 32*LAMBDA >= 256 bits: one word per chunk, C = LAMBDA)
+  static constexpr bool WIDE = (n % 32 == 0) && LAMBDA >= 8;
+  static constexpr int C = SMALL8 ? 8
+                         : ((LAMBDA < MINLANES_ && !WIDE) ? LAMBDA * ((MINLANES_ + LAMBDA - 1) / LAMBDA) : LAMBDA);
   static constexpr int CB = 4 * C;                   // chunk bytes
   static constexpr int QMAX = n >> 5;                // max whole-lane shift
   // consumer threads per CTA; 224 for lane-aligned small words (n | 32) with 48-byte chunks so
