@@ -446,3 +446,42 @@ def test_c_example_roundtrip(tmp_path, args):
     r = subprocess.run([exe, *args], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 strips differ" in r.stdout
+
+
+def _pack_words(words, n, nbytes):
+    """LSB-first bit stream of n-bit words (reading R2) -> nbytes bytes (test-local packing)."""
+    v = 0
+    for w, x in enumerate(words):
+        v |= int(x) << (w * n)
+    return np.frombuffer(v.to_bytes(nbytes, "little"), dtype=np.uint8).copy()
+
+
+def _unpack_words(buf, n, count):
+    v = int.from_bytes(bytes(buf), "little")
+    return [(v >> (w * n)) & ((1 << n) - 1) for w in range(count)]
+
+
+@pytest.mark.parametrize("p", [3, 5, 7, 11, 13, 17, 19, 29, 37, 53, 59, 61, 257, 23, 97])
+def test_rotation_unit_vectors(p):
+    """Multiplication by x^a (Eq. (powers)) on every unit vector e_b, for every
+    amount a < min(p, 64): stripe a holds only data strip a, whose word b is e_b (b < n), so the
+    encoded Q word b must equal the oracle's x^a e_b (one Sylvester step at a time) and P word b
+    must be e_b.  Checks each rotation amount and bit position (incl. the wrap into the slot
+    overflow and its reduction) in isolation."""
+    n = p - 1
+    N = min(p, 64)
+    nbytes = (n * n + 7) // 8
+    b = Batch(p, N, nbytes, N)
+    b.data.zero_()
+    unit = _pack_words([1 << w for w in range(n)], n, nbytes)
+    for a in range(N):
+        b.data[a, a, :nbytes].copy_(torch.from_numpy(unit))
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    for a in range(N):
+        Pw = _unpack_words(b.numpy_strip(a, N), n, n)
+        Qw = _unpack_words(b.numpy_strip(a, N + 1), n, n)
+        assert Pw == [1 << w for w in range(n)], a
+        for w in range(n):
+            assert Qw[w] == oracle.mul_xk(p, a, 1 << w), (p, a, w)
