@@ -707,11 +707,13 @@ __device__ __forceinline__ void build_mtab(uint2* mtab) {
 // __launch_bounds__ and the shared-memory budget per CTA (112 KB for 2, 72 KB for 3).  Measured
 // (r01 A/B): encode of 6-, 12- and 256-bit words gains from a third CTA (p = 13: 0.97 -> 1.06 of
 // the copy rate, p = 7: 0.98 -> 1.08, p = 257: 1.02 -> 1.05; 72 registers), and the NEXT-4
-// partial with it (+0-4%), while every recovery mode and the other primes' encode lose with it
+// partial (+0-4%) and NEXT-1 update (c2 +2%, c3 +11%) with it, while every recovery mode, the
+// scrub (c3 -5%) and the other primes' encode lose with it
 // (spills at 128 / 72 registers for p = 59 / 61, a 63-register cap for the 8 KiB-tile primes).
 template <int P, int MODE>
 __host__ __device__ constexpr int min_blocks() {
-  return ((P == 7 || P == 13 || P == 257) && (MODE == MODE_ENCODE || MODE == MODE_PARTIAL)) ? 3 : 2;
+  return ((P == 7 || P == 13 || P == 257) && (MODE == MODE_ENCODE || MODE == MODE_PARTIAL || MODE == MODE_UPDATE))
+             ? 3 : 2;
 }
 
 template <int P, int MODE>
