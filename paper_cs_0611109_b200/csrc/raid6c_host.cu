@@ -59,7 +59,7 @@ cudaError_t harness_fill(uint8_t* dst, uint64_t strip_stride, uint64_t stripe_st
 cudaError_t harness_count_mismatch(const uint8_t* a, const uint8_t* b, uint64_t len, uint64_t* out, cudaStream_t st);
 // NEXT-3 Reed-Solomon baseline (rs.cu)
 const void* rs_kernel_ptr(bool recover);
-size_t rs_smem_bytes();
+size_t rs_smem_bytes(bool recover);
 int rs_tile_bytes();
 int rs_chunk_bytes();
 int rs_threads();
@@ -1190,7 +1190,7 @@ static raid6c_status rs_launch(int N, size_t bytes, const uint8_t* data, size_t 
   ZP_CUDA(cudaGetDevice(&dev));
   ZP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const void* fn = zp::rs_kernel_ptr(recover);
-  raid6c_status o = kernel_occupancy(dev, fn, zp::rs_threads() + 32, zp::rs_smem_bytes(), &occ);
+  raid6c_status o = kernel_occupancy(dev, fn, zp::rs_threads() + 32, zp::rs_smem_bytes(recover), &occ);
   if (o != RAID6C_OK) return o;
   const uint64_t items = a.body_tiles * static_cast<uint64_t>(num_stripes);
   const uint64_t tail_ctas = (a.tail_units_per_stripe * static_cast<uint64_t>(num_stripes) + zp::rs_threads() - 1) /
@@ -1199,7 +1199,7 @@ static raid6c_status rs_launch(int N, size_t bytes, const uint8_t* data, size_t 
   if (grid == 0) grid = 1;
   void* args[] = {&a};
   cudaError_t e = cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(zp::rs_threads() + 32), args,
-                                   zp::rs_smem_bytes(), st);
+                                   zp::rs_smem_bytes(recover), st);
   if (tmp) cudaFreeAsync(tmp, st);
   if (e != cudaSuccess) return cuda_fail(e);
   g_launches.fetch_add(1, std::memory_order_relaxed);

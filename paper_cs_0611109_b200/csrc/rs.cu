@@ -20,8 +20,17 @@ constexpr int C = 12;           // 32-bit lanes per thread-chunk (48 B: conflict
 constexpr int CB = 4 * C;
 constexpr int THREADS = 256;
 constexpr int TB = THREADS * CB;  // 12288-byte TMA rows
-constexpr int STAGES = 7;
-constexpr size_t SMEM = (size_t)(STAGES + 2) * TB + 512 + 2 * STAGES * 8;
+// CTAs per SM and TMA stages per kernel (the Z_p kernels' occupancy rule, applied alike so the
+// comparison stays like for like): encode three CTAs x 3 stages, recovery two CTAs x 7 stages.
+#ifndef RS_ENC_MINB
+#define RS_ENC_MINB 3
+#endif
+template <bool RECOVER>
+struct Cfg {
+  static constexpr int MINB = RECOVER ? 2 : RS_ENC_MINB;
+  static constexpr int STAGES = MINB == 3 ? 3 : 7;
+  static constexpr size_t SMEM = (size_t)(STAGES + 2) * TB + 512 + 2 * STAGES * 8;
+};
 
 __device__ __forceinline__ uint32_t mul2(uint32_t v) {
   return ((v & 0x7f7f7f7fu) << 1) ^ (((v >> 7) & 0x01010101u) * 0x1du);
@@ -158,7 +167,8 @@ __device__ __forceinline__ void finish(State& st, const ZpArgs& a, const Desc& d
 }
 
 template <bool RECOVER>
-__global__ void __launch_bounds__(THREADS + 32, 2) rs_kernel(const __grid_constant__ ZpArgs a) {
+__global__ void __launch_bounds__(THREADS + 32, Cfg<RECOVER>::MINB) rs_kernel(const __grid_constant__ ZpArgs a) {
+  constexpr int STAGES = Cfg<RECOVER>::STAGES;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;
   uint8_t* outb = smem + (size_t)STAGES * TB;
@@ -270,7 +280,7 @@ __global__ void __launch_bounds__(THREADS + 32, 2) rs_kernel(const __grid_consta
 const void* rs_kernel_ptr(bool recover) {
   return recover ? reinterpret_cast<const void*>(&rs::rs_kernel<true>) : reinterpret_cast<const void*>(&rs::rs_kernel<false>);
 }
-size_t rs_smem_bytes() { return rs::SMEM; }
+size_t rs_smem_bytes(bool recover) { return recover ? rs::Cfg<true>::SMEM : rs::Cfg<false>::SMEM; }
 int rs_tile_bytes() { return rs::TB; }
 int rs_chunk_bytes() { return rs::CB; }
 int rs_threads() { return rs::THREADS; }
