@@ -329,6 +329,74 @@ def run_ours(args):
 FULL_STRIPES = {2: 256, 4: 4096, 5: 1000}  # BASELINE.json configs[1], [3], [4]: whole-config stripe counts
 
 
+def run_c1_literal(args):
+    """--config 1 --full: BASELINE.json configs[0] literally -- ONE stripe (p=5, N=4, 64 KiB, seed 0):
+    encode, then recover each of the C(6,2) = 15 erasure pairs (lost strips poisoned first) and
+    compare with the original.  The whole stripe (384 KiB) is L2-resident, so this is a latency
+    measurement (CUDA events per launch, mean over --steps repetitions), not an HBM number."""
+    import torch
+    import numpy as np
+    import synthetic
+    from paper_cs_0611109_b200 import raid6c as R
+    torch.cuda.set_device(0)
+    p, N, nbytes = 5, 4, 64 << 10
+    pb = R.parity_bytes(p, nbytes)
+    ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
+    stream = torch.cuda.Stream()
+    data = torch.empty((1, N, ss), dtype=torch.uint8, device="cuda")
+    par = torch.zeros((1, 2, ps), dtype=torch.uint8, device="cuda")
+    R.fill(data, ss, N * ss, nbytes, N, 1, 0, 1, 0, 0, 0, stream)
+    plan = R.Plan(p, N, nbytes, 0, stream)
+    a = (int(data.data_ptr()), ss, N * ss, int(par.data_ptr()), int(par.data_ptr()) + ps, 2 * ps, 1)
+    pairs = synthetic.all_pairs(N)
+    pair_dev = [torch.tensor([pr], dtype=torch.int32, device="cuda") for pr in pairs]
+    flat = lambda k: data[0, k, :nbytes] if k < N else par[0, k - N, :pb]  # noqa: E731
+    for _ in range(args.warmup):
+        plan.encode_strided(*a)
+    stream.synchronize()
+    ref = [flat(k).clone() for k in range(N + 2)]
+    reps = max(1, args.steps)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t_enc, t_rec, bad = [], {}, 0
+    with torch.cuda.stream(stream):
+        for _ in range(reps):
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            plan.encode_strided(*a)
+            e1.record(stream)
+            stream.synchronize()
+            t_enc.append(e0.elapsed_time(e1))
+            for i, pr in enumerate(pairs):
+                for k in pr:
+                    flat(k).fill_(0xA5)
+                e0, e1 = ev(), ev()
+                e0.record(stream)
+                plan.recover_strided(*a, pair_dev[i])
+                e1.record(stream)
+                stream.synchronize()
+                t_rec.setdefault(pr, []).append(e0.elapsed_time(e1))
+                bad += sum(int((flat(k) != ref[k]).sum().item()) for k in pr)
+    import oracle
+    P, Q = oracle.encode(p, synthetic.stripe_strips(0, 1, 0, N, nbytes), nbytes)
+    oracle_ok = bool(np.array_equal(ref[N].cpu().numpy(), P) and np.array_equal(ref[N + 1].cpu().numpy(), Q))
+    alg = N * nbytes + 2 * pb
+    enc_us = 1e3 * sum(t_enc) / len(t_enc)
+    rec_us = {f"{i}-{j}": round(1e3 * sum(v) / len(v), 2) for (i, j), v in t_rec.items()}
+    mean_rec = sum(rec_us.values()) / len(rec_us)
+    line = {"metric": "config 1 literal: single-stripe encode + 15 recoveries, launch latency (L2-resident)",
+            "value": round(mean_rec, 2), "unit": "us per recovery launch", "higher_is_better": False,
+            "n_gpus": 1, "steps": reps, "warmup": args.warmup, "dtype": "u32 (bitwise GF(2) words)",
+            "data": "synthetic (seed 0)", "config": {"workload": "c1 literal: p=5 N=4 64 KiB, 1 stripe, all 15 pairs",
+                                                     "l2": "384 KiB stripe: L2-resident, not an HBM number"},
+            "encode_us": round(enc_us, 2), "recover_us_per_pair": rec_us,
+            "effective_GBps": {"encode": round(alg / (enc_us * 1e-6) / 1e9, 1),
+                               "recover_mean": round(alg / (mean_rec * 1e-6) / 1e9, 1)},
+            "verified": {"bytes_differing_after_recovery": bad, "parity_matches_oracle": oracle_ok},
+            "gpu_launches": reps * (1 + len(pairs))}
+    print(json.dumps(line), flush=True)
+    plan.close()
+
+
 def run_full(args):
     """--full: the whole configuration, not one resident batch.
 
@@ -960,6 +1028,7 @@ def main():
                     help="step = encode + recover (the metric); update / scrub = NEXT-1 kernels")
     ap.add_argument("--full", action="store_true",
                     help="whole config (c4: 4096, c5: 1000, c2: 256 stripes) block-sharded over the ranks, "
+                         "c1: the literal single stripe with all 15 pairs (latency); "
                          "streamed in waves (strong scaling); --stripes overrides the total")
     ap.add_argument("--xgpu", type=int, default=0,
                     help="NEXT-4: spread each stripe's strips over G ranks (emulated on one GPU at --gpus 1)")
@@ -984,6 +1053,8 @@ def main():
         run_reference(args)
     elif args.op != "step":
         run_next1(args)
+    elif args.full and args.config == 1:
+        run_c1_literal(args)
     elif args.full:
         run_full(args)
     elif args.xgpu:

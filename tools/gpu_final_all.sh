@@ -15,6 +15,7 @@ run bench_default 900
 for c in 1 2 3 4 5; do run bench_c$c 600 --config $c --no-e2e --no-cpu-baseline; done
 for c in 2 4 5; do run full_c$c 900 --config $c --full; done
 run sweep_c3 1200 --config 3 --sweep
+run c1_literal 300 --config 1 --full --steps 5
 for op in update scrub; do for c in 1 2 3 4 5; do run next1_${op}_c$c 600 --config $c --op $op; done; done
 for spec in "2 25" "2 17" "4 115" "5 121" "3 300" "1 9"; do set -- $spec; run next2_c$1_N$2 600 --config $1 --data-strips $2 --no-e2e --no-cpu-baseline; done
 for spec in "2 16 zp --prime 17" "2 16 rs --prime 17" "2 12 zp" "2 12 rs" "4 58 zp" "4 58 rs" "5 60 zp" "5 60 rs"; do set -- $spec
