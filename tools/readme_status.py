@@ -68,6 +68,14 @@ out.append(f"c3 strip-size sweep (`bench.py --config 3 --sweep`, p=257 N=64, enc
            f"from 64 KiB to 16 MiB runs at {min(ag):.0f}–{max(ag):.0f} GB/s of algorithmic traffic "
            f"({min(fr):.3f}–{max(fr):.3f} of the measured copy rate), {min(us):.0f}–{max(us):.0f} GB/s of user data, "
            f"all oracle-checked.")
+try:
+    c1l = J("c1_literal")
+    out.append("")
+    out.append(f"Config 1 taken literally (`bench.py --config 1 --full`: ONE 64 KiB stripe, encode, then each of the 15 "
+               f"pairs rebuilt and compared; L2-resident, so a latency figure): encode {c1l['encode_us']:.1f} µs, "
+               f"recovery {c1l['value']:.1f} µs per launch on average, every pair bit-exact, parity = oracle.")
+except FileNotFoundError:
+    pass
 out.append("\n### NEXT-1 (update / scrub)\n")
 out.append("| Config | Update kernel GB/s (of measured) | Scrub kernel GB/s (of measured) |")
 out.append("|---|---|---|")
