@@ -289,7 +289,9 @@ def run_ours(args):
         d = statistics.mean(rec_ms)
         kern.append(("recover", rec_alg, d))
     dom = max(kern, key=lambda k: k[2])
-    traffic = traffic_from_profile(args.config)
+    # the committed ncu traffic belongs to the config's default launch only
+    overridden = bool(args.prime or args.data_strips or args.strip_bytes or args.stripes or rs)
+    traffic = None if overridden else traffic_from_profile(args.config)
     roof = {
         "kernel": (f"rs_kernel<{'true' if dom[0] == 'recover' else 'false'}> ({dom[0]})" if rs else
                    f"zp_kernel<{p},{1 if dom[0] == 'recover' else 0}> ({dom[0]})"),
