@@ -367,8 +367,9 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
     const uint64_t tail_ctas =
         (a.tail_units_per_stripe * static_cast<uint64_t>(a.num_stripes) + NT - 1) / NT;
     const uint64_t cap = static_cast<uint64_t>(pl->num_sms) * pl->occ[mode];
-    // body items + separate CTAs for the tail units when the launch is small enough (latency)
-    uint64_t grid = std::min<uint64_t>(cap, items + tail_ctas);
+    // a small launch gets separate CTAs for the tail units (latency); a large one is persistent
+    uint64_t grid = items < cap ? std::min<uint64_t>(cap, items + tail_ctas)
+                                : std::min<uint64_t>(cap, std::max<uint64_t>(items, tail_ctas));
     if (grid == 0) grid = 1;
     void* args[] = {&a};
     err = cudaLaunchKernel(pl->ext ? fe->kernel_ext[mode] : fe->kernel[mode], dim3(static_cast<unsigned>(grid)),

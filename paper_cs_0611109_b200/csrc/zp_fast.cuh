@@ -893,10 +893,11 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (min_blocks<P, MO
   const uint64_t tups = a.tail_units_per_stripe;
   const uint64_t tail_total = tups * static_cast<uint64_t>(a.num_stripes);
   const uint64_t body_end = tiles * TB;
-  // tail units are dealt from the LAST CTA down: in a small launch (fewer body items than CTAs) the
-  // extra CTAs at the end of the grid take them at once, in parallel with the body items
-  for (uint64_t u = static_cast<uint64_t>(gridDim.x - 1 - blockIdx.x) * NT + tid; u < tail_total;
-       u += static_cast<uint64_t>(gridDim.x) * NT) {
+  // in a small launch (fewer body items than CTAs) the tail units are dealt from the LAST CTA down,
+  // so the extra CTAs at the end of the grid take them at once, in parallel with the body items;
+  // in a large one from the first CTA up (measured 1-2 % better there)
+  const uint64_t tail_rank = gridDim.x > body_items ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+  for (uint64_t u = tail_rank * NT + tid; u < tail_total; u += static_cast<uint64_t>(gridDim.x) * NT) {
     const int s = static_cast<int>(u / tups);
     const uint64_t roff = body_end + (u - static_cast<uint64_t>(s) * tups) * CB;  // row offset
     const uint64_t off = obase + roff;                                           // strip offset
