@@ -1,5 +1,6 @@
 // raid6c_host.cu -- host side of libraid6c: argument validation, plans, kernel selection and
-// launch, the host-buffer streaming pipeline, and the C ABI entry points of include/raid6c.h.
+// launch, and the core C ABI entry points of include/raid6c.h (the host-buffer pipeline, NEXT-3
+// and NEXT-4 entry points live in host_pipeline.cu, rs_host.cu and xgpu_host.cu).
 // Every byte of the method is computed by the sm_100a kernels (zp_fast.cuh / zp_generic.cu);
 // there is no CPU fallback anywhere in this file.
 #include <algorithm>
@@ -15,8 +16,7 @@
 
 #include <cuda_runtime.h>
 
-#include "raid6c.h"
-#include "zp_args.h"
+#include "host_internal.h"
 
 namespace zp {
 // fast-path instantiations (zp_fast_p*.cu)
@@ -53,19 +53,10 @@ const FastEntry* fast_entry(int p) {
   }
 }
 
-cudaError_t harness_fill(uint8_t* dst, uint64_t strip_stride, uint64_t stripe_stride, uint64_t len, int nstrips,
-                         int nstripes, uint64_t seed, int cfg, int stripe0, int strip0, int sparse_mode,
-                         cudaStream_t st);
-cudaError_t harness_count_mismatch(const uint8_t* a, const uint8_t* b, uint64_t len, uint64_t* out, cudaStream_t st);
-// NEXT-3 Reed-Solomon baseline (rs.cu)
-const void* rs_kernel_ptr(bool recover);
-size_t rs_smem_bytes(bool recover);
-int rs_tile_bytes();
-int rs_chunk_bytes();
-int rs_threads();
 }  // namespace zp
 
-namespace {
+namespace zp {
+namespace host {
 
 std::atomic<uint64_t> g_launches{0};
 thread_local std::string g_last_err;
@@ -74,11 +65,6 @@ raid6c_status cuda_fail(cudaError_t e) {
   g_last_err = cudaGetErrorString(e);
   return RAID6C_E_CUDA;
 }
-#define ZP_CUDA(call)                              \
-  do {                                             \
-    cudaError_t e_ = (call);                       \
-    if (e_ != cudaSuccess) return cuda_fail(e_);   \
-  } while (0)
 
 bool is_valid_p(int p) {
   if (p < 3 || p > RAID6C_MAX_P || (p % 2) == 0) return false;
@@ -220,50 +206,6 @@ raid6c_status kernel_occupancy(int device, const void* fn, int threads, size_t s
   return RAID6C_OK;
 }
 
-}  // namespace
-
-struct raid6c_plan_s {
-  int p = 0, N = 0;
-  size_t bytes = 0, pbytes = 0;
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  const zp::FastEntry* fe = nullptr;
-  int num_sms = 148;
-  int occ[6] = {1, 1, 1, 1, 1, 1};  // CTAs per SM per kernel mode
-  bool ext = false;           // N > p: extended code of Eq. (qext)
-  std::mutex mu;              // serialises the shared single-stripe plans' program buffer
-  zp::ExtProg* d_prog = nullptr;
-  size_t prog_cap = 0;
-  int2* d_er = nullptr;
-  size_t er_cap = 0;
-  // d_er / d_prog are rewritten by later calls, possibly on another stream (plan_set_stream):
-  // the last launch that reads them records this event, and every rewrite waits for it
-  cudaEvent_t tables_done = nullptr;
-  bool tables_pending = false;
-  raid6c_status sticky = RAID6C_OK;
-  // host-buffer pipeline
-  uint8_t* d_stage = nullptr;
-  size_t slot_bytes = 0;
-  int slot_stripes = 0;
-  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // in, kernel, out
-  cudaEvent_t ev_in[2] = {}, ev_k[2] = {}, ev_out[2] = {};
-  bool host_ready = false;
-  uint64_t h2d = 0, d2h = 0;
-};
-
-namespace {
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 raid6c_status build_prog_table(raid6c_plan pl);
 
@@ -618,190 +560,10 @@ raid6c_status cached_plan(int p, int N, size_t bytes, raid6c_plan* out) {
   return RAID6C_OK;
 }
 
-// ------------------------------------------------------------------ host-buffer pipeline
-raid6c_status host_setup(raid6c_plan pl, int num_stripes) {
-  DeviceGuard g(pl->device);
-  const size_t sd = (pl->bytes + 255) / 256 * 256, sp = (pl->pbytes + 255) / 256 * 256;
-  const size_t stripe_dev = static_cast<size_t>(pl->N) * sd + 2 * sp;
-  const size_t target = size_t(512) << 20;
-  int cs = static_cast<int>(std::max<size_t>(1, target / stripe_dev));
-  cs = std::min(cs, std::max(1, num_stripes));
-  const size_t need = static_cast<size_t>(cs) * stripe_dev;
-  if (!pl->host_ready) {
-    for (int i = 0; i < 3; i++) ZP_CUDA(cudaStreamCreateWithFlags(&pl->hs[i], cudaStreamNonBlocking));
-    for (int i = 0; i < 2; i++) {
-      ZP_CUDA(cudaEventCreateWithFlags(&pl->ev_in[i], cudaEventDisableTiming));
-      ZP_CUDA(cudaEventCreateWithFlags(&pl->ev_k[i], cudaEventDisableTiming));
-      ZP_CUDA(cudaEventCreateWithFlags(&pl->ev_out[i], cudaEventDisableTiming));
-    }
-    pl->host_ready = true;
-  }
-  if (pl->slot_bytes < need || pl->slot_stripes < cs) {
-    if (pl->d_stage) {
-      ZP_CUDA(cudaDeviceSynchronize());
-      cudaFree(pl->d_stage);
-      pl->d_stage = nullptr;
-    }
-    ZP_CUDA(cudaMalloc(&pl->d_stage, 2 * need));
-    pl->slot_bytes = need;
-    pl->slot_stripes = cs;
-  }
-  return RAID6C_OK;
-}
+}  // namespace host
+}  // namespace zp
 
-// Copy `rows` strips of `width` bytes: host rows at src + r*spitch -> device rows at dst + r*dpitch.
-raid6c_status copy_rows(uint8_t* dst, size_t dpitch, const uint8_t* src, size_t spitch, size_t width, int rows,
-                        cudaMemcpyKind kind, cudaStream_t st) {
-  if (rows <= 0) return RAID6C_OK;
-  if (rows == 1) {
-    ZP_CUDA(cudaMemcpyAsync(dst, src, width, kind, st));
-  } else {
-    ZP_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, st));
-  }
-  return RAID6C_OK;
-}
-
-raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_t stripe_stride, uint8_t* P,
-                       uint8_t* Q, size_t parity_stride, int num_stripes, const raid6c_erasure* er,
-                       int num_erasures, bool recover) {
-  if (!pl) return RAID6C_E_NULL;
-  if (num_stripes < 0) return RAID6C_E_SIZE;
-  if (num_stripes == 0) return RAID6C_OK;
-  if (!data || !P || !Q) return RAID6C_E_NULL;
-  if (pl->N > 1 && strip_stride < pl->bytes) return RAID6C_E_SIZE;
-  if (num_stripes > 1 && (stripe_stride < pl->bytes || parity_stride < pl->pbytes)) return RAID6C_E_SIZE;
-  std::vector<int2> pairs;
-  if (recover) {
-    if (!er) return RAID6C_E_NULL;
-    if (num_erasures != 1 && num_erasures != num_stripes) return RAID6C_E_SIZE;
-    pairs.resize(num_stripes);
-    for (int s = 0; s < num_stripes; s++) {
-      const raid6c_erasure& e = er[num_erasures == 1 ? 0 : s];
-      raid6c_status c = check_erasure(pl->N, e.lost_i, e.lost_j);
-      if (c != RAID6C_OK) return c;
-      pairs[s] = make_int2(std::min(e.lost_i, e.lost_j), std::max(e.lost_i, e.lost_j));
-    }
-  }
-  raid6c_status st = host_setup(pl, num_stripes);
-  if (st != RAID6C_OK) return st;
-  DeviceGuard g(pl->device);
-  const int N = pl->N;
-  const size_t sd = (pl->bytes + 255) / 256 * 256, sp = (pl->pbytes + 255) / 256 * 256;
-  const int cs = pl->slot_stripes;
-  cudaStream_t s_in = pl->hs[0], s_k = pl->hs[1], s_out = pl->hs[2];
-  if (recover) {
-    // per-stripe pairs for the whole call, uploaded once on the kernel stream
-    std::vector<raid6c_erasure> ev(num_stripes);
-    for (int s = 0; s < num_stripes; s++) ev[s] = {pairs[s].x, pairs[s].y};
-    st = upload_erasures(pl, ev.data(), num_stripes, s_k);
-    if (st != RAID6C_OK) return st;
-  }
-  // order after anything already queued on the plan stream
-  ZP_CUDA(cudaEventRecord(pl->ev_out[0], pl->stream));
-  ZP_CUDA(cudaStreamWaitEvent(s_in, pl->ev_out[0], 0));
-  ZP_CUDA(cudaEventRecord(pl->ev_out[1], pl->stream));
-  uint64_t h2d = 0, d2h = 0;
-  int c = 0;
-  for (int s0 = 0; s0 < num_stripes; s0 += cs, c++) {
-    const int slot = c & 1;
-    const int ns = std::min(cs, num_stripes - s0);
-    uint8_t* base = pl->d_stage + static_cast<size_t>(slot) * pl->slot_bytes;
-    uint8_t* dP = base + static_cast<size_t>(cs) * N * sd;
-    uint8_t* dQ = dP + static_cast<size_t>(cs) * sp;
-    const size_t dstripe = static_cast<size_t>(N) * sd;
-    if (c >= 2) ZP_CUDA(cudaStreamWaitEvent(s_in, pl->ev_out[slot], 0));
-    // ---- H2D of the inputs
-    for (int i = 0; i < ns; i++) {
-      const int s = s0 + i;
-      const uint8_t* hd = data + static_cast<size_t>(s) * stripe_stride;
-      uint8_t* dd = base + static_cast<size_t>(i) * dstripe;
-      int x = N, y = N + 1;
-      if (recover) { x = pairs[s].x; y = pairs[s].y; }
-      // contiguous runs of surviving data strips
-      int k = 0;
-      while (k < N) {
-        if (k == x || k == y) { k++; continue; }
-        int e = k;
-        while (e < N && e != x && e != y) e++;
-        st = copy_rows(dd + static_cast<size_t>(k) * sd, sd, hd + static_cast<size_t>(k) * strip_stride, strip_stride,
-                       pl->bytes, e - k, cudaMemcpyHostToDevice, s_in);
-        if (st != RAID6C_OK) return st;
-        h2d += static_cast<uint64_t>(e - k) * pl->bytes;
-        k = e;
-      }
-      if (recover && x != N && y != N) {
-        ZP_CUDA(cudaMemcpyAsync(dP + static_cast<size_t>(i) * sp, P + static_cast<size_t>(s) * parity_stride, pl->pbytes,
-                                cudaMemcpyHostToDevice, s_in));
-        h2d += pl->pbytes;
-      }
-      if (recover && y != N + 1) {
-        ZP_CUDA(cudaMemcpyAsync(dQ + static_cast<size_t>(i) * sp, Q + static_cast<size_t>(s) * parity_stride, pl->pbytes,
-                                cudaMemcpyHostToDevice, s_in));
-        h2d += pl->pbytes;
-      }
-    }
-    ZP_CUDA(cudaEventRecord(pl->ev_in[slot], s_in));
-    // ---- kernel
-    ZP_CUDA(cudaStreamWaitEvent(s_k, pl->ev_in[slot], 0));
-    zp::ZpArgs a;
-    std::memset(&a, 0, sizeof(a));
-    for (int k = 0; k < N; k++) a.base[k] = base + static_cast<size_t>(k) * sd;
-    a.base[N] = dP;
-    a.base[N + 1] = dQ;
-    a.data_stride = dstripe;
-    a.parity_stride = sp;
-    a.num_stripes = ns;
-    a.ei = N;
-    a.ej = N + 1;
-    if (recover) {
-      a.er = pl->d_er + s0;
-      a.er_stride = 1;
-      if (pl->ext) a.prog = pl->d_prog;
-    }
-    st = launch(pl, a, recover ? zp::KMODE_RECOVER : zp::KMODE_ENCODE, s_k);
-    if (st != RAID6C_OK) return st;
-    ZP_CUDA(cudaEventRecord(pl->ev_k[slot], s_k));
-    // ---- D2H of the outputs
-    ZP_CUDA(cudaStreamWaitEvent(s_out, pl->ev_k[slot], 0));
-    if (!recover) {
-      st = copy_rows(P + static_cast<size_t>(s0) * parity_stride, parity_stride, dP, sp, pl->pbytes, ns,
-                     cudaMemcpyDeviceToHost, s_out);
-      if (st != RAID6C_OK) return st;
-      st = copy_rows(Q + static_cast<size_t>(s0) * parity_stride, parity_stride, dQ, sp, pl->pbytes, ns,
-                     cudaMemcpyDeviceToHost, s_out);
-      if (st != RAID6C_OK) return st;
-      d2h += 2ull * ns * pl->pbytes;
-    } else {
-      for (int i = 0; i < ns; i++) {
-        const int s = s0 + i;
-        const int lost[2] = {pairs[s].x, pairs[s].y};
-        for (int q = 0; q < 2; q++) {
-          const int k = lost[q];
-          if (k < N) {
-            ZP_CUDA(cudaMemcpyAsync(data + static_cast<size_t>(s) * stripe_stride + static_cast<size_t>(k) * strip_stride,
-                                    base + static_cast<size_t>(i) * dstripe + static_cast<size_t>(k) * sd, pl->bytes,
-                                    cudaMemcpyDeviceToHost, s_out));
-            d2h += pl->bytes;
-          } else {
-            uint8_t* hdst = (k == N ? P : Q) + static_cast<size_t>(s) * parity_stride;
-            const uint8_t* dsrc = (k == N ? dP : dQ) + static_cast<size_t>(i) * sp;
-            ZP_CUDA(cudaMemcpyAsync(hdst, dsrc, pl->pbytes, cudaMemcpyDeviceToHost, s_out));
-            d2h += pl->pbytes;
-          }
-        }
-      }
-    }
-    ZP_CUDA(cudaEventRecord(pl->ev_out[slot], s_out));
-  }
-  ZP_CUDA(cudaStreamSynchronize(s_out));
-  ZP_CUDA(cudaStreamSynchronize(s_k));
-  ZP_CUDA(cudaGetLastError());
-  pl->h2d = h2d;
-  pl->d2h = d2h;
-  return RAID6C_OK;
-}
-
-}  // namespace
+using namespace zp::host;
 
 // ====================================================================== C ABI
 extern "C" {
@@ -994,253 +756,6 @@ raid6c_status raid6c_update_strided(raid6c_plan plan, uint8_t* data, size_t stri
     a.upd_stride = 2;
   }
   return launch(plan, a, zp::KMODE_UPDATE, plan->stream);
-}
-
-// ---------------------------------------------------------------- NEXT-4: cross-GPU stripe layout
-size_t raid6c_xgpu_range_bytes(int p, size_t bytes, int num_ranks) {
-  if (!is_valid_p(p) || bytes == 0 || num_ranks < 1 || num_ranks > RAID6C_MAX_RANKS) return 0;
-  const uint64_t gr = range_granule_p(p);
-  const uint64_t units = (parity_bytes(p, bytes) + gr - 1) / gr;
-  return static_cast<size_t>(((units + num_ranks - 1) / num_ranks) * gr);
-}
-
-// Strip table of a cross-GPU call: N+2 global-index pointers, strides.
-static raid6c_status xgpu_args(raid6c_plan plan, const uint8_t* const* strips, size_t data_stride, size_t parity_stride,
-                               int num_stripes, int k_lo, int k_hi, zp::ZpArgs& a) {
-  if (!plan || !strips) return RAID6C_E_NULL;
-  if (num_stripes < 0) return RAID6C_E_SIZE;
-  if (k_lo < 0 || k_hi > plan->N + 2 || k_lo > k_hi) return RAID6C_E_INVALID_INDEX;
-  for (int k = k_lo; k < k_hi; k++)
-    if (!strips[k]) return RAID6C_E_NULL;
-  if (num_stripes > 1 && (data_stride < plan->bytes || parity_stride < plan->pbytes)) return RAID6C_E_SIZE;
-  std::memset(&a, 0, sizeof(a));
-  for (int k = 0; k < plan->N + 2; k++) a.base[k] = strips[k];
-  a.data_stride = data_stride;
-  a.parity_stride = parity_stride;
-  a.num_stripes = num_stripes;
-  a.ei = plan->N;  // encode = the PQ pair
-  a.ej = plan->N + 1;
-  a.k_lo = k_lo;
-  a.k_hi = k_hi;
-  return RAID6C_OK;
-}
-
-raid6c_status raid6c_partial_strided(raid6c_plan plan, const uint8_t* const* strips, size_t data_stride,
-                                     size_t parity_stride, int num_stripes, const raid6c_erasure* erasures,
-                                     int num_erasures, int erasures_on_device, int k_lo, int k_hi, int num_ranges,
-                                     uint8_t* const* part_p, uint8_t* const* part_q, size_t part_stride,
-                                     size_t range_bytes) {
-  zp::ZpArgs a;
-  raid6c_status st = xgpu_args(plan, strips, data_stride, parity_stride, num_stripes, k_lo, k_hi, a);
-  if (st != RAID6C_OK) return st;
-  if (num_ranges < 1 || num_ranges > RAID6C_MAX_RANKS) return RAID6C_E_SIZE;
-  if (!part_p || !part_q) return RAID6C_E_NULL;
-  const uint64_t gr = range_granule(plan);
-  if (range_bytes == 0 || range_bytes % gr != 0 || static_cast<uint64_t>(range_bytes) * num_ranges < plan->pbytes)
-    return RAID6C_E_SIZE;
-  if (num_stripes > 1 && part_stride < range_bytes) return RAID6C_E_SIZE;
-  const int used = static_cast<int>((plan->pbytes + range_bytes - 1) / range_bytes);  // ranges holding bytes
-  for (int g = 0; g < used; g++)
-    if (!part_p[g] || !part_q[g]) return RAID6C_E_NULL;
-  for (int g = 0; g < num_ranges; g++) {
-    a.part_p[g] = part_p[g];
-    a.part_q[g] = part_q[g];
-  }
-  a.nranges = used;
-  a.range_bytes = range_bytes;
-  a.part_stride = part_stride;
-  DeviceGuard g(plan->device);
-  if (erasures) {
-    st = set_erasures(plan, a, erasures, num_erasures, erasures_on_device, num_stripes, false);
-    if (st != RAID6C_OK) return st;
-  }
-  return launch(plan, a, zp::KMODE_PARTIAL, plan->stream);
-}
-
-raid6c_status raid6c_combine_strided(raid6c_plan plan, uint8_t* const* strips, size_t data_stride,
-                                     size_t parity_stride, int num_stripes, const raid6c_erasure* erasures,
-                                     int num_erasures, int erasures_on_device, int num_sources,
-                                     const uint8_t* const* src_p, const uint8_t* const* src_q, size_t part_stride,
-                                     size_t range_lo, size_t range_hi) {
-  zp::ZpArgs a;
-  raid6c_status st = xgpu_args(plan, strips, data_stride, parity_stride, num_stripes, 0, 0, a);
-  if (st != RAID6C_OK) return st;
-  if (num_sources < 1 || num_sources > RAID6C_MAX_RANKS) return RAID6C_E_SIZE;
-  if (!src_p || !src_q) return RAID6C_E_NULL;
-  for (int r = 0; r < num_sources; r++) {
-    if (!src_p[r] || !src_q[r]) return RAID6C_E_NULL;
-    a.src_p[r] = src_p[r];
-    a.src_q[r] = src_q[r];
-  }
-  const uint64_t gr = range_granule(plan);
-  if (range_lo % gr != 0 || range_hi < range_lo || range_hi > plan->pbytes) return RAID6C_E_SIZE;
-  if (num_stripes > 1 && part_stride < range_hi - range_lo) return RAID6C_E_SIZE;
-  a.nsrc = num_sources;
-  a.range_lo = range_lo;
-  a.range_hi = range_hi;
-  a.part_stride = part_stride;
-  DeviceGuard g(plan->device);
-  if (erasures) {
-    st = set_erasures(plan, a, erasures, num_erasures, erasures_on_device, num_stripes, true);
-    if (st != RAID6C_OK) return st;
-  }
-  // output strips of every stripe must be present: check against the (host-known) pairs
-  if (!erasures || !erasures_on_device) {
-    for (int s = 0; s < (erasures ? num_erasures : 1); s++) {
-      const int x = erasures ? std::min(erasures[s].lost_i, erasures[s].lost_j) : plan->N;
-      const int y = erasures ? std::max(erasures[s].lost_i, erasures[s].lost_j) : plan->N + 1;
-      if (!strips[x] || !strips[y]) return RAID6C_E_NULL;
-    }
-  }
-  return launch_combine(plan, a, plan->stream);
-}
-
-raid6c_status raid6c_dev_alloc(size_t bytes, int device, void** dev_ptr) {
-  if (!dev_ptr) return RAID6C_E_NULL;
-  *dev_ptr = nullptr;
-  if (bytes == 0) return RAID6C_E_SIZE;
-  DeviceGuard g(device);
-  ZP_CUDA(cudaMalloc(dev_ptr, bytes));
-  return RAID6C_OK;
-}
-
-raid6c_status raid6c_dev_free(void* dev_ptr) {
-  if (!dev_ptr) return RAID6C_E_NULL;
-  ZP_CUDA(cudaFree(dev_ptr));
-  return RAID6C_OK;
-}
-
-raid6c_status raid6c_ipc_export(const void* dev_ptr, uint8_t handle[64]) {
-  if (!dev_ptr || !handle) return RAID6C_E_NULL;
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "CUDA IPC handles are 64 bytes");
-  cudaIpcMemHandle_t h;
-  ZP_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
-  std::memcpy(handle, &h, 64);
-  return RAID6C_OK;
-}
-
-raid6c_status raid6c_ipc_open(const uint8_t handle[64], int device, void** dev_ptr) {
-  if (!handle || !dev_ptr) return RAID6C_E_NULL;
-  *dev_ptr = nullptr;
-  DeviceGuard g(device);
-  cudaIpcMemHandle_t h;
-  std::memcpy(&h, handle, 64);
-  ZP_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
-  return RAID6C_OK;
-}
-
-raid6c_status raid6c_ipc_close(void* dev_ptr) {
-  if (!dev_ptr) return RAID6C_E_NULL;
-  ZP_CUDA(cudaIpcCloseMemHandle(dev_ptr));
-  return RAID6C_OK;
-}
-
-// ---------------------------------------------------------------- NEXT-3: GF(256) RS baseline
-static raid6c_status rs_launch(int N, size_t bytes, const uint8_t* data, size_t strip_stride, size_t stripe_stride,
-                               const uint8_t* P, const uint8_t* Q, size_t parity_stride, int num_stripes, bool recover,
-                               const raid6c_erasure* er, int num_er, int er_on_device, cudaStream_t st) {
-  if (N < 1 || N > 255) return RAID6C_E_INVALID_N;
-  if (bytes == 0 || num_stripes < 0) return RAID6C_E_SIZE;
-  if (!data || !P || !Q) return RAID6C_E_NULL;
-  if (N > 1 && strip_stride < bytes) return RAID6C_E_SIZE;
-  if (num_stripes > 1 && (stripe_stride < bytes || parity_stride < bytes)) return RAID6C_E_SIZE;
-  if (num_stripes == 0) return RAID6C_OK;
-  zp::ZpArgs a;
-  std::memset(&a, 0, sizeof(a));
-  for (int k = 0; k < N; k++) a.base[k] = data + static_cast<size_t>(k) * strip_stride;
-  a.base[N] = P;
-  a.base[N + 1] = Q;
-  a.data_stride = stripe_stride;
-  a.parity_stride = parity_stride;
-  a.bytes = a.pbytes = bytes;
-  a.N = N;
-  a.num_stripes = num_stripes;
-  a.ei = N;
-  a.ej = N + 1;
-  int2* tmp = nullptr;
-  if (recover) {
-    if (!er) return RAID6C_E_NULL;
-    if (num_er != 1 && num_er != num_stripes) return RAID6C_E_SIZE;
-    if (er_on_device) {
-      a.er = reinterpret_cast<const int2*>(er);
-      a.er_stride = num_er == 1 ? 0 : 1;
-    } else {
-      std::vector<int2> h(num_er);
-      for (int s = 0; s < num_er; s++) {
-        raid6c_status c = check_erasure(N, er[s].lost_i, er[s].lost_j);
-        if (c != RAID6C_OK) return c;
-        h[s] = make_int2(std::min(er[s].lost_i, er[s].lost_j), std::max(er[s].lost_i, er[s].lost_j));
-      }
-      if (num_er == 1) {
-        a.ei = h[0].x;
-        a.ej = h[0].y;
-      } else {
-        ZP_CUDA(cudaMallocAsync(&tmp, num_er * sizeof(int2), st));
-        ZP_CUDA(cudaMemcpyAsync(tmp, h.data(), num_er * sizeof(int2), cudaMemcpyHostToDevice, st));
-        a.er = tmp;
-        a.er_stride = 1;
-      }
-    }
-  }
-  bool aligned = true;
-  for (int k = 0; k < N + 2; k++) aligned &= (reinterpret_cast<uintptr_t>(a.base[k]) & 15u) == 0;
-  if (num_stripes > 1) aligned &= (stripe_stride % 16 == 0) && (parity_stride % 16 == 0);
-  const uint64_t TB = zp::rs_tile_bytes(), CB = zp::rs_chunk_bytes();
-  a.body_tiles = aligned ? bytes / TB : 0;
-  a.tail_units_per_stripe = (bytes - a.body_tiles * TB + CB - 1) / CB;
-  int dev = 0, sms = 148, occ = 1;
-  ZP_CUDA(cudaGetDevice(&dev));
-  ZP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const void* fn = zp::rs_kernel_ptr(recover);
-  raid6c_status o = kernel_occupancy(dev, fn, zp::rs_threads() + 32, zp::rs_smem_bytes(recover), &occ);
-  if (o != RAID6C_OK) return o;
-  const uint64_t items = a.body_tiles * static_cast<uint64_t>(num_stripes);
-  const uint64_t tail_ctas = (a.tail_units_per_stripe * static_cast<uint64_t>(num_stripes) + zp::rs_threads() - 1) /
-                             zp::rs_threads();
-  uint64_t grid = std::min<uint64_t>(static_cast<uint64_t>(sms) * occ, std::max<uint64_t>(items, tail_ctas));
-  if (grid == 0) grid = 1;
-  void* args[] = {&a};
-  cudaError_t e = cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(zp::rs_threads() + 32), args,
-                                   zp::rs_smem_bytes(recover), st);
-  if (tmp) cudaFreeAsync(tmp, st);
-  if (e != cudaSuccess) return cuda_fail(e);
-  g_launches.fetch_add(1, std::memory_order_relaxed);
-  return RAID6C_OK;
-}
-
-raid6c_status raid6c_rs_encode_strided(int N, size_t bytes, const uint8_t* data, size_t strip_stride,
-                                       size_t stripe_stride, uint8_t* P, uint8_t* Q, size_t parity_stride,
-                                       int num_stripes, void* stream) {
-  return rs_launch(N, bytes, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, false, nullptr, 0,
-                   0, static_cast<cudaStream_t>(stream));
-}
-
-raid6c_status raid6c_rs_recover_strided(int N, size_t bytes, uint8_t* data, size_t strip_stride, size_t stripe_stride,
-                                        uint8_t* P, uint8_t* Q, size_t parity_stride, int num_stripes,
-                                        const raid6c_erasure* erasures, int num_erasures, int erasures_on_device,
-                                        void* stream) {
-  return rs_launch(N, bytes, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, true, erasures,
-                   num_erasures, erasures_on_device, static_cast<cudaStream_t>(stream));
-}
-
-raid6c_status raid6c_encode_host(raid6c_plan plan, const uint8_t* data, size_t strip_stride, size_t stripe_stride,
-                                 uint8_t* P, uint8_t* Q, size_t parity_stride, int num_stripes) {
-  return host_run(plan, const_cast<uint8_t*>(data), strip_stride, stripe_stride, P, Q, parity_stride, num_stripes,
-                  nullptr, 0, false);
-}
-
-raid6c_status raid6c_recover_host(raid6c_plan plan, uint8_t* data, size_t strip_stride, size_t stripe_stride,
-                                  uint8_t* P, uint8_t* Q, size_t parity_stride, int num_stripes,
-                                  const raid6c_erasure* erasures, int num_erasures) {
-  return host_run(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, erasures, num_erasures,
-                  true);
-}
-
-raid6c_status raid6c_host_traffic(raid6c_plan plan, uint64_t* h2d_bytes, uint64_t* d2h_bytes) {
-  if (!plan || !h2d_bytes || !d2h_bytes) return RAID6C_E_NULL;
-  *h2d_bytes = plan->h2d;
-  *d2h_bytes = plan->d2h;
-  return RAID6C_OK;
 }
 
 raid6c_status raid6c_fill(uint8_t* dst, size_t strip_stride, size_t stripe_stride, size_t len, int nstrips,
