@@ -966,7 +966,7 @@ def _oracle_work(p, N, nbytes, cfg, sparse_mode, budget_s, max_threads):
     u0, t0 = task(0)
     per = max(t0, 1e-3)
     ntasks = max(threads, int(budget_s * threads / per))
-    ntasks = min(ntasks, 4 * threads)
+    ntasks = min(ntasks, 16 * threads)  # ~budget_s of wall time on the host cores
     t_start = time.perf_counter()
     users = 0
     with cf.ThreadPoolExecutor(max_workers=threads) as ex:
