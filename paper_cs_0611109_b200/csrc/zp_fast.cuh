@@ -496,14 +496,15 @@ __device__ __forceinline__ void mul_prog(const uint32_t (&t)[G::C], const ExtPro
 
 // Evaluation plan for the geometric series S_M = sum_{m<M} b^m of the DD solve, by a per-lane
 // cost model (rotation ~4 ops, reduction ~6 ops): the doubling chain costs a rotation and a
-// reduction per step; a two-level split M = M1*M2 + R costs M2 + M1 + R rotations and two
-// reductions (one if M2 == M).  p = 5, 13: direct (3 / 7 rot + 1 red); 17: 3x3; 59: 5x6;
-// 61, 257: chain (8 steps).
+// reduction per step; a two-level split M = M1*M2 + R costs (M2-1) + (M1-1) + R rotations and
+// two reductions (M-1 and one if M2 == M).  p = 3, 5, 7: direct; 13: 3x2+1 (c2 recovery +0.3%
+// over direct); 17: 3x3; 59: 5x6; 61, 257: chain (8 steps).
 constexpr int c_popcount(int v) { return v == 0 ? 0 : (v & 1) + c_popcount(v >> 1); }
 template <int M>
 struct SeriesPlan {
+  // rotations by x^0 (the first term of each level) are free XORs: only the others count
   static constexpr int cost2(int m2) {
-    return m2 >= M ? 4 * M + 6 : 4 * (m2 + M / m2 + M % m2) + 12;
+    return m2 >= M ? 4 * (M - 1) + 6 : 4 * ((m2 - 1) + (M / m2 - 1) + M % m2) + 12;
   }
   static constexpr int best_m2() {
     int best = M, bc = cost2(M);
