@@ -60,6 +60,21 @@ def slot_stride(range_bytes: int, align: int = 256) -> int:
     return (range_bytes + align - 1) // align * align
 
 
+def arena_layout(rank: int, world: int, N: int, S: int, strip_stride: int, parity_stride: int,
+                 slot_pstride: int) -> dict:
+    """Byte layout of rank's IPC arena (xgpu.Distributed): its strips [k_lo, k_hi) for S stripes
+    (strip k of stripe s at strip_off[k] + s * stride(k)), then its 2 * world partial slots
+    (source r's dP / dQ slot at slot_off + (2r + which) * S * slot_pstride)."""
+    k_lo, k_hi = strip_block(rank, world, N)
+    off, strip_off = 0, {}
+    for k in range(k_lo, k_hi):
+        strip_off[k] = off
+        off += S * (strip_stride if k < N else parity_stride)
+    slot_off = off
+    off += world * 2 * S * slot_pstride
+    return {"strip_off": strip_off, "slot_off": slot_off, "size": max(off, 256)}
+
+
 def alg_bytes(N: int, nbytes: int, pbytes: int, world: int, rank: int, range_bytes: int,
               pairs=None) -> dict:
     """Algorithmic bytes per stripe of one rank's two launches (DESIGN.md NEXT-4):
@@ -156,14 +171,7 @@ class Distributed:
         self._flag = torch.zeros(1, dtype=torch.int32, device=torch.device("cuda", device))
 
     def _arena_layout(self, r):
-        k_lo, k_hi = self.blocks[r]
-        off, strip_off = 0, {}
-        for k in range(k_lo, k_hi):
-            strip_off[k] = off
-            off += self.S * (self.ss if k < self.N else self.ps)
-        slot_off = off
-        off += self.G * 2 * self.S * self.pstride
-        return {"strip_off": strip_off, "slot_off": slot_off, "size": max(off, 256)}
+        return arena_layout(r, self.G, self.N, self.S, self.ss, self.ps, self.pstride)
 
     def slot(self, owner, src, which):
         """Address of owner's slot for source rank `src` (which: 0 = dP, 1 = dQ)."""

@@ -154,3 +154,28 @@ def test_gloo_world2_partial_syndromes_sum_and_solve():
         assert pr.exitcode == 0
     for rank, ok in res:
         assert ok and all(ok), (rank, ok)
+
+
+def test_arena_layouts_hold_every_strip_once_and_slots_do_not_overlap():
+    """xgpu.Distributed's IPC arenas: every global strip lives in exactly one rank's arena, all
+    regions are 16-byte aligned (TMA), and strips and slots never overlap."""
+    from paper_cs_0611109_b200 import xgpu
+    for N, G, S in [(12, 4, 3), (58, 8, 2), (4, 3, 5), (300, 8, 1), (2, 4, 2)]:
+        ss, ps, pst = 4096, 4352, xgpu.slot_stride(1000)
+        held = {}
+        for r in range(G):
+            lay = xgpu.arena_layout(r, G, N, S, ss, ps, pst)
+            regions = []
+            for k, off in lay["strip_off"].items():
+                assert k not in held
+                held[k] = r
+                regions.append((off, off + S * (ss if k < N else ps)))
+            for src in range(G):
+                for which in (0, 1):
+                    o = lay["slot_off"] + (2 * src + which) * S * pst
+                    regions.append((o, o + S * pst))
+            regions.sort()
+            assert all(a % 16 == 0 for a, _ in regions)
+            assert all(b <= c for (_, b), (c, _) in zip(regions, regions[1:]))
+            assert regions[-1][1] <= lay["size"]
+        assert sorted(held) == list(range(N + 2))
