@@ -111,6 +111,88 @@ __global__ void __launch_bounds__(CONS + 32, 2) tma_read_kernel(const uint8_t* b
   if (acc == 0x9e3779b9u) sink[0] = acc;
 }
 
+// ------------------------------------------------------------------ (3) TMA read K rows, bulk-store W rows
+// The product kernels' memory pattern without their arithmetic: per tile, K rows in through the
+// mbarrier ring, XOR-folded in registers, the fold stored to W strips (STORE: SMEM-staged bulk store or st.global from registers).
+template <int STORE>  // 0: SMEM-staged bulk store, 1: st.global.v4 from registers, 2: st.global.cs.v4
+__global__ void __launch_bounds__(CONS + 32, 2) tma_mix_kernel(const uint8_t* base, uint64_t strip_stride, int K,
+                                                                uint8_t* obase, int W, uint64_t tiles) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* obuf = smem + ST * TB;
+  uint64_t* full = reinterpret_cast<uint64_t*>(obuf + TB);
+  uint64_t* empty = full + ST;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < ST; s++) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty[s])), "r"(CONS / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == CONS / 32) {
+    if (lane == 0) {
+      uint32_t stage = 0, ph = 0;
+      for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x)
+        for (int k = 0; k < K; k++) {
+          asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W_%=;\n\t}"
+                       ::"r"(smem_u32(&empty[stage])), "r"(ph ^ 1u) : "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(TB) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(smem_u32(smem + stage * TB)), "l"(base + k * strip_stride + t * TB), "r"(TB),
+                       "r"(smem_u32(&full[stage])) : "memory");
+          if (++stage == ST) { stage = 0; ph ^= 1u; }
+        }
+    }
+    return;
+  }
+  uint32_t stage = 0, ph = 0;
+  for (uint64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    uint4 a[3] = {};
+    for (int k = 0; k < K; k++) {
+      asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@!P1 bra W_%=;\n\t}"
+                   ::"r"(smem_u32(&full[stage])), "r"(ph) : "memory");
+      const uint4* row = reinterpret_cast<const uint4*>(smem + stage * TB);
+#pragma unroll
+      for (int j = 0; j < 3; j++) {
+        const uint4 v = row[tid + j * CONS];
+        a[j].x ^= v.x; a[j].y ^= v.y; a[j].z ^= v.z; a[j].w ^= v.w;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[stage])) : "memory");
+      if (++stage == ST) { stage = 0; ph ^= 1u; }
+    }
+    if (W == 0) {
+      if ((a[0].x ^ a[1].y ^ a[2].z) == 0x9e3779b9u) obase[0] = 1;
+      continue;
+    }
+    if (STORE != 0) {
+      for (int w = 0; w < W; w++) {
+        uint4* o = reinterpret_cast<uint4*>(obase + w * strip_stride + t * TB);
+#pragma unroll
+        for (int j = 0; j < 3; j++) {
+          if (STORE == 1) o[tid + j * CONS] = a[j];
+          else __stcs(o + tid + j * CONS, a[j]);
+        }
+      }
+      continue;
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(CONS) : "memory");
+#pragma unroll
+    for (int j = 0; j < 3; j++) reinterpret_cast<uint4*>(obuf)[tid + j * CONS] = a[j];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(CONS) : "memory");
+    if (tid == 0) {
+      for (int w = 0; w < W; w++)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(obase + w * strip_stride + t * TB),
+                     "r"(smem_u32(obuf)), "r"(TB) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void ldg_read_kernel(const uint4* src, uint64_t n16, uint32_t* sink) {
   uint32_t acc = 0;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
@@ -170,7 +252,7 @@ int main() {
   const int Ks[5] = {1, 4, 12, 58, 66};
   for (int i = 0; i < 5; i++) {
     const int K = Ks[i];
-    // same total bytes per point (~3.2 GB): repeat the K strips' tiles over the whole buffer
+    // same total bytes per point (415 MB): repeat the K strips' tiles over the whole buffer
     const uint64_t tiles_k = (Kmax * tiles) / K;
     float best = 1e30f;
     for (int rep = 0; rep < 5; rep++) {
@@ -200,8 +282,46 @@ int main() {
     }
     printf(" \"ldg128_read_GBps\": %.1f,\n", Kmax * strip / (best / 1e3) / 1e9);
   }
+  {
+    // read:write mixes of the configs (K strips in, W strips out per tile): 415 MB read per point
+    uint8_t* obuf;
+    CK(cudaMalloc(&obuf, 2 * Kmax * strip));
+    const size_t msmem = ST * TB + TB + 2 * ST * 8;
+    CK(cudaFuncSetAttribute(tma_mix_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
+    CK(cudaFuncSetAttribute(tma_mix_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
+    CK(cudaFuncSetAttribute(tma_mix_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(msmem)));
+    const int mixes[8][2] = {{1, 1}, {2, 2}, {4, 2}, {6, 0}, {8, 2}, {12, 2}, {16, 2}, {58, 2}};
+    const char* sname[3] = {"bulk_store", "st_global", "st_global_cs"};
+    printf(" \"tma_read_K_store_W_GBps\": {");
+    for (int m = 0; m < 3; m++) {
+      printf("%s\"%s\": {", m ? ", " : "", sname[m]);
+      for (int i = 0; i < 8; i++) {
+        const int K = mixes[i][0], W = mixes[i][1];
+        if (W == 0 && m) continue;
+        const uint64_t tiles_m = (Kmax * tiles) / K;  // the whole input buffer read once, W rows per tile out
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; rep++) {
+          CK(cudaEventRecord(e0));
+          if (m == 0) tma_mix_kernel<0><<<sms * 2, CONS + 32, msmem>>>(buf, tiles_m * TB, K, obuf, W, tiles_m);
+          if (m == 1) tma_mix_kernel<1><<<sms * 2, CONS + 32, msmem>>>(buf, tiles_m * TB, K, obuf, W, tiles_m);
+          if (m == 2) tma_mix_kernel<2><<<sms * 2, CONS + 32, msmem>>>(buf, tiles_m * TB, K, obuf, W, tiles_m);
+          CK(cudaEventRecord(e1));
+          CK(cudaEventSynchronize(e1));
+          float ms;
+          CK(cudaEventElapsedTime(&ms, e0, e1));
+          if (ms < best) best = ms;
+        }
+        const double bytes = static_cast<double>(K + W) * tiles_m * TB;
+        printf("%s\"%d:%d\": %.1f", i ? ", " : "", K, W, bytes / (best / 1e3) / 1e9);
+      }
+      printf("}");
+    }
+    printf("},\n");
+    CK(cudaFree(obuf));
+  }
   printf(" \"how\": \"tools/microbench.cu: int ops = 8 independent chains x 32 warps/SM, clock64 cycles (best of 3); "
          "TMA = cp.async.bulk 12 KiB rows from K strips round-robin, 8-stage mbarrier ring, 2 CTAs/SM, no compute, "
-         "~3.2 GB per point, best of 5 (CUDA events)\"}\n");
+         "415 MB read per point, best of 5 (CUDA events); K:W = the same ring + XOR fold, fold bulk-stored from SMEM or stored from registers (st.global, st.global.cs) to W strips, "
+         "GB/s counts (K+W) rows per tile\"}\n");
   return 0;
 }
