@@ -32,6 +32,21 @@ const FastEntry* fast_entry_13();
 const FastEntry* fast_entry_17();
 const FastEntry* fast_entry_59();
 const FastEntry* fast_entry_61();
+const FastEntry* fast_entry_23();
+const FastEntry* fast_entry_31();
+const FastEntry* fast_entry_41();
+const FastEntry* fast_entry_43();
+const FastEntry* fast_entry_47();
+const FastEntry* fast_entry_73();
+const FastEntry* fast_entry_89();
+const FastEntry* fast_entry_97();
+const FastEntry* fast_entry_101();
+const FastEntry* fast_entry_109();
+const FastEntry* fast_entry_113();
+const FastEntry* fast_entry_137();
+const FastEntry* fast_entry_193();
+const FastEntry* fast_entry_233();
+const FastEntry* fast_entry_241();
 const FastEntry* fast_entry_257();
 
 const FastEntry* fast_entry(int p) {
@@ -48,6 +63,21 @@ const FastEntry* fast_entry(int p) {
     case 17: return fast_entry_17();
     case 59: return fast_entry_59();
     case 61: return fast_entry_61();
+    case 23: return fast_entry_23();
+    case 31: return fast_entry_31();
+    case 41: return fast_entry_41();
+    case 43: return fast_entry_43();
+    case 47: return fast_entry_47();
+    case 73: return fast_entry_73();
+    case 89: return fast_entry_89();
+    case 97: return fast_entry_97();
+    case 101: return fast_entry_101();
+    case 109: return fast_entry_109();
+    case 113: return fast_entry_113();
+    case 137: return fast_entry_137();
+    case 193: return fast_entry_193();
+    case 233: return fast_entry_233();
+    case 241: return fast_entry_241();
     case 257: return fast_entry_257();
     default: return nullptr;
   }

@@ -76,8 +76,11 @@ struct Geo {
   static constexpr int CB = 4 * C;                   // chunk bytes
   static constexpr int QMAX = n >> 5;                // max whole-lane shift
   // consumer threads per CTA; 224 for lane-aligned small words (n | 32) with 48-byte chunks so
-  // that the tiles (10752 B) leave a 1.5% instead of 6% ragged tail on 64 KiB strips (config 1)
-  static constexpr int THREADS = SMALL8 ? 256 : (C >= 24 ? 128 : ((32 % n == 0) ? 224 : 256));
+  // that the tiles (10752 B) leave a 1.5% instead of 6% ragged tail on 64 KiB strips (config 1);
+  // 128 for chunks of 20 lanes or more (two CTAs of 160 threads keep 168 registers each: with 256
+  // the 96-register cap spills, measured p = 23 / 47 / 89 encode 0.74-0.82 -> 0.97-1.00 and
+  // recovery 0.50-0.56 -> 0.76-0.95 of the copy rate; p = 43: encode 1.05 -> 0.98, recovery 0.74 -> 0.78)
+  static constexpr int THREADS = SMALL8 ? 256 : (C >= 20 ? 128 : ((32 % n == 0) ? 224 : 256));
   static constexpr int TB = THREADS * CB;            // TMA row (tile) bytes
   static constexpr int MTAB = (n + 1) * LAMBDA;      // mask table entries (uint2)
   static_assert(LAMBDA <= 32, "fast path needs a period of at most 32 lanes");

@@ -18,7 +18,8 @@ from tests.gpu_util import Batch  # noqa: E402
 
 PRIMES = [p for p in range(3, 258) if all(p % q for q in range(2, int(p ** 0.5) + 1))]
 
-FAST = [3, 5, 7, 11, 13, 17, 19, 29, 37, 53, 59, 61, 257]
+FAST = [3, 5, 7, 11, 13, 17, 19, 29, 37, 53, 59, 61, 257,
+        23, 31, 41, 43, 47, 73, 89, 97, 101, 109, 113, 137, 193, 233, 241]
 
 
 def _case(seed):

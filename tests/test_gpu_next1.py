@@ -18,7 +18,8 @@ from tests.gpu_util import Batch  # noqa: E402
 
 CASES = [(13, 12, 3 * 12288 + 777, 3, 0), (5, 4, 65536, 3, 0), (59, 58, 2 * 14848 + 50, 2, 0),
          (61, 60, 2 * 15360 + 9, 2, 0), (257, 64, 2 * 8192 + 33, 2, 0), (17, 16, 12000, 2, 0),
-         (11, 10, 2000, 2, 0), (23, 22, 2000, 2, 0), (13, 12, 5000, 2, 3), (3, 3, 1000, 2, 0), (7, 7, 777, 3, 1)]
+         (11, 10, 2000, 2, 0), (23, 22, 2000, 2, 0), (13, 12, 5000, 2, 3), (3, 3, 1000, 2, 0), (7, 7, 777, 3, 1),
+         (67, 30, 3000, 2, 0)] + [(p, min(p - 1, 30), 2 * 16384 + 77, 2, 0) for p in (23, 31, 41, 47, 73, 97, 113, 233, 241)]
 
 
 def _np(t):

@@ -17,10 +17,12 @@ import synthetic  # noqa: E402
 from paper_cs_0611109_b200 import raid6c as R  # noqa: E402
 from tests.gpu_util import Batch  # noqa: E402
 
-# (p, N, bytes, stripes); fast-path primes and generic ones (23, 43)
+# (p, N, bytes, stripes); fast-path primes and a generic one (67)
 CASES = [(5, 9, 3 * 10752 + 517, 2), (13, 25, 2 * 12288 + 99, 2), (13, 17, 5000, 2), (17, 33, 11000, 2),
          (59, 90, 14848 + 333, 2), (61, 121, 15360 + 17, 2), (257, 300, 8192 + 64, 1), (11, 21, 3000, 2),
-         (19, 37, 1500, 2), (23, 45, 1500, 2), (43, 60, 1200, 2)]
+         (19, 37, 1500, 2), (23, 45, 1500, 2), (43, 60, 1200, 2), (23, 30, 3 * 16384 + 99, 2),
+         (41, 51, 3 * 16384 + 5, 2), (47, 60, 2 * 16384 + 1, 2), (89, 100, 16384 + 77, 1), (101, 120, 4000, 1),
+         (233, 240, 3000, 1), (241, 300, 2000, 1), (67, 80, 1000, 1)]
 
 
 def _np(t):

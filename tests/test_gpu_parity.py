@@ -21,8 +21,9 @@ import synthetic  # noqa: E402
 from paper_cs_0611109_b200 import raid6c as R  # noqa: E402
 from tests.gpu_util import Batch, segment_bounds  # noqa: E402
 
-FAST = [3, 5, 7, 11, 13, 17, 19, 29, 37, 53, 59, 61, 257]
-GENERIC = [23, 31, 41, 43, 47, 67, 97, 127]
+FAST = [3, 5, 7, 11, 13, 17, 19, 29, 37, 53, 59, 61, 257,
+        23, 31, 41, 43, 47, 73, 89, 97, 101, 109, 113, 137, 193, 233, 241]
+GENERIC = [67, 71, 79, 83, 103, 127, 131, 251]  # period lcm(n, 32) above 32 lanes
 
 
 def _poison(b, s, ks):
@@ -91,7 +92,8 @@ def test_recover_single_all_pairs(p, N, nbytes):
                                           (59, 58, 3 * 14848 + 99, 2), (61, 60, 2 * 15360 + 7, 2),
                                           (257, 64, 3 * 8192 + 5000, 2), (3, 3, 12288 * 3 + 1, 2),
                                           (17, 16, 12288 * 2 + 30, 2), (7, 6, 12288 * 2 + 13, 2),
-                                          (19, 18, 9000, 2)])
+                                          (19, 18, 9000, 2)] +
+                         [(p, min(p - 1, 40), 3 * 16384 + 1001, 2) for p in FAST[13:]])
 def test_batch_encode_and_mixed_recover(p, N, nbytes, S):
     b = Batch(p, N, nbytes, S)
     b.fill_synthetic(seed=1, cfg=9, stripe0=0)
@@ -362,7 +364,7 @@ def test_pipeline_race_stress(p, N, nbytes, S):
             assert np.array_equal(_np(b.par[s, 1, b0:b0 + Q.size]), Q)
 
 
-@pytest.mark.parametrize("p", [5, 13, 17, 59, 61, 257, 11, 97])
+@pytest.mark.parametrize("p", [5, 13, 17, 59, 61, 257, 11, 67] + FAST[13:])
 def test_dd_solve_every_z(p):
     """The DD solve (1 + x^z)^{-1} (reading R11) for every z = y - x in
     1..N-1 with N = p - 1 data strips, at varying x (the rotation origin): one stripe per z,
@@ -370,7 +372,7 @@ def test_dd_solve_every_z(p):
     against the oracle first; the rebuilt strips must equal the originals."""
     N = p - 1
     nbytes = {5: 10752 + 333, 13: 12288 + 333, 17: 10752 + 77, 59: 14848 + 333, 61: 15360 + 333,
-              257: 8192 + 96, 11: 3000, 97: 2000}[p]
+              257: 8192 + 96, 11: 3000, 67: 2000}.get(p, 16384 + 333)
     zs = list(range(1, N))
     S = len(zs)
     b = Batch(p, N, nbytes, S)
@@ -461,7 +463,7 @@ def _unpack_words(buf, n, count):
     return [(v >> (w * n)) & ((1 << n) - 1) for w in range(count)]
 
 
-@pytest.mark.parametrize("p", [3, 5, 7, 11, 13, 17, 19, 29, 37, 53, 59, 61, 257, 23, 97])
+@pytest.mark.parametrize("p", FAST + [67, 127, 251])
 def test_rotation_unit_vectors(p):
     """Multiplication by x^a (Eq. (powers)) on every unit vector e_b, for every
     amount a < min(p, 64): stripe a holds only data strip a, whose word b is e_b (b < n), so the

@@ -32,7 +32,8 @@ CASES = [(13, 12, 3 * 12288 + 1001, 3, 4), (13, 12, 3 * 12288 + 1001, 3, 1), (5,
          (59, 58, 2 * 14848 + 333, 2, 8), (61, 60, 2 * 15360 + 17, 2, 5), (257, 64, 3 * 4096 + 64, 2, 8),
          (17, 16, 2 * 10752 + 9, 2, 2), (3, 2, 5000, 3, 4), (7, 6, 4000, 2, 3), (11, 10, 3000, 2, 3),
          (19, 18, 2500, 2, 4), (13, 25, 2 * 12288 + 99, 2, 4), (59, 90, 14848 + 333, 1, 6),
-         (23, 22, 3000, 2, 3), (67, 40, 2000, 2, 4), (43, 60, 1500, 1, 5)]
+         (23, 22, 3000, 2, 3), (67, 40, 2000, 2, 4), (43, 60, 1500, 1, 5), (41, 40, 2 * 16384 + 33, 2, 3),
+         (47, 46, 2 * 16384 + 5, 2, 5), (89, 60, 16384 + 77, 2, 4), (233, 100, 16384 + 77, 1, 4), (71, 30, 2000, 2, 3)]
 
 
 def _np(t):
