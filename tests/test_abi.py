@@ -43,6 +43,13 @@ def test_valid_p_and_fast_set():
         assert R.valid_p(q) == (q in primes and q >= 3 and q <= 257)
     for q in [5, 13, 59, 61, 257]:
         assert R.has_fast_path(q)
+    # the fast (compile-time-p) kernel exists for exactly the primes whose period lcm(p-1, 32)
+    # fits 32 lanes; the others run the generic kernel
+    from math import gcd
+    fits = [q for q in primes if (q - 1) // gcd(q - 1, 32) <= 32]
+    assert len(fits) == 28 and len(primes) - len(fits) == 26
+    for q in primes:
+        assert R.has_fast_path(q) == (q in fits), q
 
 
 def test_ext_supported_matches_oracle():

@@ -73,7 +73,10 @@ try:
     out.append("")
     out.append(f"Config 1 taken literally (`bench.py --config 1 --full`: ONE 64 KiB stripe, encode, then each of the 15 "
                f"pairs rebuilt and compared; L2-resident, so a latency figure): encode {c1l['encode_us']:.1f} µs, "
-               f"recovery {c1l['value']:.1f} µs per launch on average, every pair bit-exact, parity = oracle.")
+               f"recovery {c1l['value']:.1f} µs per call on average (from Python, host path included)"
+               + (f", {c1l['cuda_graph']['us_per_launch']:.1f} µs per launch on the device when the 16 calls are "
+                  f"replayed from a CUDA graph" if (c1l.get('cuda_graph') or {}).get('us_per_launch') else "")
+               + "; every pair bit-exact, parity = oracle.")
 except FileNotFoundError:
     pass
 out.append("\n### NEXT-1 (update / scrub)\n")
