@@ -267,58 +267,6 @@ __device__ __forceinline__ void rot_dispatch(int key, const uint32_t (&S)[G::C],
   }
 }
 
-// rot_body with the whole-lane shifts q, qp applied at run time by a barrel shifter over the
-// chunk's lanes (log2(QMAX+1) select stages each way) instead of a compiled body per (q, qp):
-// one body per call site instead of up to (QMAX+1)^2 (ZP_BARREL_QMIN: an A/B experiment).
-template <class G>
-__device__ __forceinline__ void rot_barrel(const uint32_t (&S)[G::C], int q, int qp, uint32_t r, uint32_t rp,
-                                           const uint2* __restrict__ mrow, Acc<G>& acc) {
-  constexpr int C = G::C;
-  constexpr int STG = top_bit(G::QMAX) + 1;
-  uint32_t Sx[C + 1];  // Sx[l] = S[l - q] (0 outside the chunk)
-#pragma unroll
-  for (int l = 0; l < C; l++) Sx[l] = S[l];
-  Sx[C] = 0u;
-#pragma unroll
-  for (int st = 0; st < STG; st++) {
-    const bool on = (q >> st) & 1;
-#pragma unroll
-    for (int l = C; l >= 0; l--) {
-      const uint32_t v = (l >= (1 << st)) ? Sx[l >= (1 << st) ? l - (1 << st) : 0] : 0u;
-      Sx[l] = on ? v : Sx[l];
-    }
-  }
-#pragma unroll
-  for (int l = 0; l < C; l++) {
-    const uint2 m = mrow[l % G::LAMBDA];
-    const uint32_t X = __funnelshift_l(l >= 1 ? Sx[l >= 1 ? l - 1 : 0] : 0u, Sx[l], r);
-    acc.ax[l] ^= X & m.x;
-  }
-  acc.tc ^= __funnelshift_l(Sx[C - 1], Sx[C], r);
-  uint32_t Sy[C + 1];  // Sy[l] = S[l + qp] (0 outside the chunk)
-#pragma unroll
-  for (int l = 0; l < C; l++) Sy[l] = S[l];
-  Sy[C] = 0u;
-#pragma unroll
-  for (int st = 0; st < STG; st++) {
-    const bool on = (qp >> st) & 1;
-#pragma unroll
-    for (int l = 0; l <= C; l++) {
-      const uint32_t v = (l + (1 << st) <= C) ? Sy[l + (1 << st) <= C ? l + (1 << st) : 0] : 0u;
-      Sy[l] = on ? v : Sy[l];
-    }
-  }
-#pragma unroll
-  for (int l = 0; l < C; l++) {
-    const uint2 m = mrow[l % G::LAMBDA];
-    acc.ay[l] ^= __funnelshift_r(Sy[l], Sy[l + 1], rp) & m.y;
-  }
-}
-
-#ifndef ZP_BARREL_QMIN
-#define ZP_BARREL_QMIN 1000
-#endif
-
 // acc += x^a * S   (a in [0, p), S reduced or not: only its n stream bits are used)
 template <class G>
 __device__ __forceinline__ void rot_acc(const uint32_t (&S)[G::C], int a, const uint2* __restrict__ mtab, Acc<G>& acc) {
@@ -329,11 +277,7 @@ __device__ __forceinline__ void rot_acc(const uint32_t (&S)[G::C], int a, const 
   }
   const int q = a >> 5, qp = (G::P - a) >> 5;
   const uint32_t r = static_cast<uint32_t>(a & 31), rp = static_cast<uint32_t>((G::P - a) & 31);
-  if constexpr (G::QMAX >= ZP_BARREL_QMIN && !G::WIDE) {
-    rot_barrel<G>(S, q, qp, r, rp, mtab + a * G::LAMBDA, acc);
-  } else {
-    rot_dispatch<G, 0>(q * (G::QMAX + 1) + qp, S, r, rp, mtab + a * G::LAMBDA, acc);
-  }
+  rot_dispatch<G, 0>(q * (G::QMAX + 1) + qp, S, r, rp, mtab + a * G::LAMBDA, acc);
 }
 
 // V = pi(acc): the reduced n-bit stream of the accumulated R' value.
