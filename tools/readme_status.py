@@ -79,6 +79,20 @@ try:
                + "; every pair bit-exact, parity = oracle.")
 except FileNotFoundError:
     pass
+try:
+    with open(os.path.join(os.path.dirname(D.rstrip("/")), "r01_primes.json")) as f:
+        pr = json.load(f)
+    fp = pr["fast_path"]
+    enc = [v["encode"]["frac"] for v in fp.values()]
+    rec = [v["recover"]["frac"] for v in fp.values()]
+    gen = [v[k]["frac"] for v in pr["generic_path"].values() for k in ("encode", "recover")]
+    out.append("")
+    out.append(f"Other primes (`profiles/r01_primes.json`, c2 shape N = 12, 4 MiB × 256): the {len(fp)} primes added to the "
+               f"fast path this round (every prime whose period lcm(p−1, 32) fits 32 lanes) encode at "
+               f"{min(enc):.2f}–{max(enc):.2f} and recover at {min(rec):.2f}–{max(rec):.2f} of the copy rate; "
+               f"primes on the generic kernel (p = 67, 127 measured) run at {min(gen):.3f}–{max(gen):.3f}.")
+except FileNotFoundError:
+    pass
 out.append("\n### NEXT-1 (update / scrub)\n")
 out.append("| Config | Update kernel GB/s (of measured) | Scrub kernel GB/s (of measured) |")
 out.append("|---|---|---|")
