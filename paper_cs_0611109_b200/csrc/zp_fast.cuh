@@ -79,7 +79,8 @@ struct Geo {
   // that the tiles (10752 B) leave a 1.5% instead of 6% ragged tail on 64 KiB strips (config 1);
   // 128 for chunks of 20 lanes or more (two CTAs of 160 threads keep 168 registers each: with 256
   // the 96-register cap spills, measured p = 23 / 47 / 89 encode 0.74-0.82 -> 0.97-1.00 and
-  // recovery 0.50-0.56 -> 0.76-0.95 of the copy rate; p = 43: encode 1.05 -> 0.98, recovery 0.74 -> 0.78)
+  // recovery 0.50-0.56 -> 0.76-0.95 of the copy rate; p = 43: encode 1.05 -> 0.98, recovery 0.74 -> 0.78);
+  // not below 20 lanes: 128 threads for p = 73, 97, 113, 137, 193, 241 (12-18 lanes) cost recovery 11-31 %
   static constexpr int THREADS = SMALL8 ? 256 : (C >= 20 ? 128 : ((32 % n == 0) ? 224 : 256));
   static constexpr int TB = THREADS * CB;            // TMA row (tile) bytes
   static constexpr int MTAB = (n + 1) * LAMBDA;      // mask table entries (uint2)
