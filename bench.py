@@ -299,7 +299,10 @@ def run_ours(args):
         "traffic": traffic.get(dom[0]) if isinstance(traffic, dict) else None,
         "alg_bytes_per_launch": dom[1], "avg_launch_ms": round(dom[2], 4),
     }
+    launch_ms = {"encode": enc_ms, "recover": rec_ms}  # per timed step, this rank
     per_kernel = {k[0]: {"alg_bytes": k[1], "avg_ms": round(k[2], 4),
+                         "median_ms": round(statistics.median(launch_ms[k[0]]), 4),
+                         "best_ms": round(min(launch_ms[k[0]]), 4),
                          "achieved_GBps": round(k[1] / (k[2] / 1e3) / 1e9, 1),
                          "frac_of_peak": round(k[1] / (k[2] / 1e3) / 1e9 / peak, 4),
                          "frac_of_8TBps": round(k[1] / (k[2] / 1e3) / 1e9 / 8000.0, 4),
