@@ -1,18 +1,24 @@
-// zp_generic.cu -- runtime-p Z_p-RAID kernel (any odd prime p <= 257) for primes without a
-// compile-time specialisation (zp_fast.cuh).  Same mathematics, simpler mapping:
-//   * one thread per byte-aligned group of g = 8/gcd(n,8) words (so outputs are whole bytes
-//     and no two threads touch the same byte);
-//   * each word is held as a p-bit value in NL = ceil(p/32) 32-bit limbs (NL is a template
-//     parameter, p a runtime value; slot bit p-1 = the R' overflow), extracted from the strip
-//     with funnel-shifted 32-bit reads; multiplication by x^a is a rotation of the p-bit slot
-//     done limb-wise (a funnel-shift stage plus a log2(NL)-step limb barrel shifter with
-//     static register indexing); the reduction pi is deferred to the end of each sum
-//     (DESIGN.md "kernels");
+// zp_generic.cu -- Z_p-RAID kernel for the primes without a fast (TMA) specialisation
+// (zp_fast.cuh needs a period lcm(p-1, 32) of at most 32 lanes; the other 26 odd primes <= 257
+// run here).  Same mathematics, simpler mapping:
+//   * one thread per byte-aligned group of g = 8/gcd(n,8) words (GB = g*n/8 bytes, so outputs
+//     are whole bytes and no two threads touch the same byte); p is a template parameter, so
+//     the group geometry, every word's bit offset and the limb count NL = ceil(p/32) are
+//     compile-time;
+//   * per strip, the group's GB bytes are read with aligned 32-bit loads (realigned by one
+//     funnel shift) and the g words are cut out at compile-time offsets; each word is held as
+//     a p-bit value in NL 32-bit limbs (slot bit p-1 = the R' overflow); multiplication by x^a
+//     is a rotation of the p-bit slot done limb-wise (a funnel-shift stage plus a log2(NL)-step
+//     limb barrel shifter with static register indexing); the reduction pi is deferred to the
+//     end of each sum;
 //   * the class epilogues are the same as the fast path (Lemma 23.2 proof PAPER.md:380-401,
-//     Sec. 4.6), the DD inverse by the same doubling chain.
-// No TMA and no shared memory: the path for primes outside the fast set.
+//     Sec. 4.6), the DD inverse by the same doubling chain; outputs are
+//     packed at compile-time offsets and written with aligned 32-bit stores (byte stores only
+//     at the group's edges).
+// No TMA and no shared memory.
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "zp_args.h"
@@ -39,29 +45,6 @@ __device__ __forceinline__ void wxor(Word<NL>& a, const Word<NL>& b) {
 __device__ __forceinline__ uint32_t low_mask(int bits, int i) {
   const int r = bits - 32 * i;
   return r >= 32 ? 0xFFFFFFFFu : (r <= 0 ? 0u : ((1u << r) - 1u));
-}
-
-// 32 bits of the strip starting at bit `pos` (zero past `len` bytes).
-__device__ __forceinline__ uint32_t read32(const uint8_t* g, uint64_t len, uint64_t pos) {
-  const uint64_t w4 = pos >> 5;
-  if ((reinterpret_cast<uintptr_t>(g) & 3u) == 0 && 4 * w4 + 8 <= len) {
-    const uint32_t* g4 = reinterpret_cast<const uint32_t*>(g);
-    return __funnelshift_r(__ldg(g4 + w4), __ldg(g4 + w4 + 1), static_cast<uint32_t>(pos & 31));
-  }
-  const uint64_t b = pos >> 3;
-  uint64_t v = 0;
-#pragma unroll
-  for (int i = 0; i < 5; i++)
-    if (b + i < len) v |= static_cast<uint64_t>(__ldg(g + b + i)) << (8 * i);
-  return static_cast<uint32_t>(v >> (pos & 7));
-}
-
-// Word w (n bits at stream bit w*n) of a strip of `len` bytes.
-template <int NL>
-__device__ __forceinline__ void load_word(const uint8_t* g, uint64_t len, uint64_t w, int n, Word<NL>& out) {
-  const uint64_t b0 = w * static_cast<uint64_t>(n);
-#pragma unroll
-  for (int i = 0; i < NL; i++) out.v[i] = (32 * i < n && (b0 >> 3) < len) ? (read32(g, len, b0 + 32 * i) & low_mask(n, i)) : 0u;
 }
 
 // out = in << s (s < 32*NL), bits beyond 32*NL dropped.
@@ -187,7 +170,15 @@ __device__ __forceinline__ uint64_t rlen(const ZpArgs& a, int k) {
   return (k == K_NEW || k < a.N) ? a.bytes : a.pbytes;
 }
 
-constexpr int GROUP_MAX_WORDS32 = 33;  // g*n/8 <= n/2 <= 128 bytes (+1 limb of spill)
+// Compile-time group geometry of prime P.
+template <int P>
+struct GP {
+  static constexpr int n = P - 1;
+  static constexpr int NL = (P + 31) / 32;                                  // limbs per p-bit slot
+  static constexpr int g = 8 / ((n & 7) == 0 ? 8 : ((n & 3) == 0 ? 4 : 2));  // words per group
+  static constexpr int GB = g * n / 8;                                      // bytes per group
+  static constexpr int W4 = (GB + 3) / 4;                                   // 32-bit words per group
+};
 
 // Group range of one launch: all groups of the strip, or (combine) the groups of bytes
 // [range_lo, range_hi) -- range_lo is a multiple of the group size (host-checked).
@@ -205,40 +196,248 @@ __device__ __forceinline__ void group_span(const ZpArgs& a, int mode, int n, int
   }
 }
 
-// buf (group bit stream) |= word v at bit offset o.
-template <int NL>
-__device__ __forceinline__ void put_word(uint32_t* buf, const Word<NL>& v, int o, int n) {
+// buf[0..W4) = bytes [byte0, byte0 + 4*W4) of a row of `len` bytes, zero past `len`
+// (reading R5's zero extension); buf[W4] = 0.
+template <int W4>
+__device__ __forceinline__ void load_group(const uint8_t* row, uint64_t len, uint64_t byte0, uint32_t (&buf)[W4 + 1]) {
+  const uint8_t* pg = row + byte0;
+  const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(pg) & 3u);
+  buf[W4] = 0u;
+  if (byte0 + 4 * W4 + 4 <= len + mis) {  // the aligned words [pg - mis, pg - mis + 4(W4+1)) lie in the row
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(pg - mis);
+    uint32_t raw[W4 + 1];
 #pragma unroll
-  for (int i = 0; i < NL; i++) {
-    if (32 * i >= n) break;
-    const int pos = o + 32 * i, idx = pos >> 5, sh = pos & 31;
-    buf[idx] |= v.v[i] << sh;
-    if (sh) buf[idx + 1] |= v.v[i] >> (32 - sh);
+    for (int i = 0; i <= W4; i++) raw[i] = __ldg(q + i);
+#pragma unroll
+    for (int i = 0; i < W4; i++) buf[i] = __funnelshift_r(raw[i], raw[i + 1], 8 * mis);
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < W4; i++) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int b = 0; b < 4; b++)
+      if (byte0 + 4 * i + b < len) v |= static_cast<uint32_t>(__ldg(pg + 4 * i + b)) << (8 * b);
+    buf[i] = v;
   }
 }
 
+// Word WI of the group (bits [WI*n, WI*n + n) of buf), compile-time offsets.
+template <int P, int WI>
+__device__ __forceinline__ void group_word(const uint32_t (&buf)[GP<P>::W4 + 1], Word<GP<P>::NL>& out) {
+  constexpr int n = GP<P>::n;
+#pragma unroll
+  for (int i = 0; i < GP<P>::NL; i++) {
+    const int pos = WI * n + 32 * i, idx = pos >> 5, sh = pos & 31;
+    const uint32_t lo = idx < GP<P>::W4 + 1 ? buf[idx < GP<P>::W4 + 1 ? idx : 0] : 0u;
+    const uint32_t hi = idx + 1 < GP<P>::W4 + 1 ? buf[idx + 1 < GP<P>::W4 + 1 ? idx + 1 : 0] : 0u;
+    out.v[i] = 32 * i < n ? (__funnelshift_r(lo, hi, sh) & low_mask(n, i)) : 0u;
+  }
+}
+
+// ob |= word v at bit offset WI*n (compile-time).
+template <int P, int WI>
+__device__ __forceinline__ void group_put(uint32_t (&ob)[GP<P>::W4 + 1], const Word<GP<P>::NL>& v) {
+  constexpr int n = GP<P>::n;
+#pragma unroll
+  for (int i = 0; i < GP<P>::NL; i++) {
+    if (32 * i >= n) break;
+    const int pos = WI * n + 32 * i, idx = pos >> 5, sh = pos & 31;
+    if (idx < GP<P>::W4 + 1) ob[idx < GP<P>::W4 + 1 ? idx : 0] |= v.v[i] << sh;
+    if (sh && idx + 1 < GP<P>::W4 + 1) ob[idx + 1 < GP<P>::W4 + 1 ? idx + 1 : 0] |= v.v[i] >> (32 - sh);
+  }
+}
+
+// Bytes [0, nb) of the group buffer to dst: aligned 32-bit stores, byte stores at the edges.
+template <int W4>
+__device__ __forceinline__ void store_group(uint8_t* dst, int nb, const uint32_t (&ob)[W4 + 1]) {
+  const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 3u);
+  uint32_t* q = reinterpret_cast<uint32_t*>(dst - mis);
+#pragma unroll
+  for (int j = 0; j <= W4; j++) {  // word j of q holds group bytes [4j - mis, 4j - mis + 4)
+    const uint32_t v = __funnelshift_l(j > 0 ? ob[j > 0 ? j - 1 : 0] : 0u, ob[j], 8 * mis);
+    const int b0 = 4 * j - static_cast<int>(mis);
+    if (b0 >= 0 && b0 + 4 <= nb) {
+      q[j] = v;
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; b++)
+        if (b0 + b >= 0 && b0 + b < nb) dst[b0 + b] = static_cast<uint8_t>(v >> (8 * b));
+    }
+  }
+}
+
+// Class epilogue of one word: o[0..nout) from the folded Pa / acc (and NEWW for the update).
 template <int NL>
-__global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int mode) {
-  const int n = p - 1;
-  const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);  // 8 / gcd(n, 8)
-  const int gbytes = g * n / 8;
-  const int glimbs = (gbytes + 3) / 4;
+__device__ __forceinline__ void finish_word(const ZpArgs& a, const Desc& d, int p, int mode, bool ext, Word<NL>& Pa,
+                                            Word<NL>& acc, const Word<NL>& NEWW, Word<NL> (&o)[3], bool valid,
+                                            uint32_t& bad) {
+  const ExtProg* pr = ext ? a.prog + pair_index(d.x, d.y, a.N) : nullptr;
+  if (mode == KMODE_PARTIAL) {  // unsolved partial syndromes (NEXT-4)
+    o[0] = Pa;
+    reduce(acc, p);
+    o[1] = acc;
+  } else if (ext && (d.cls == 1 || d.cls == 2 || d.cls == 3)) {  // extended code (Lemma 23.2 with Eq. (qext))
+    if (d.cls == 1) {
+      o[0] = Pa;
+      add_coeff(acc, Pa, d.x, p);
+      reduce(acc, p);
+      o[1] = acc;
+    } else if (d.cls == 2) {
+      reduce(acc, p);
+      mul_prog(acc, pr, p, o[0]);
+      o[1] = Pa;
+      wxor(o[1], o[0]);
+    } else {
+      add_coeff(acc, Pa, d.x, p);
+      reduce(acc, p);
+      mul_prog(acc, pr, p, o[1]);
+      o[0] = o[1];
+      wxor(o[0], Pa);
+    }
+  } else if (d.cls == 0) {
+    o[0] = Pa;
+    reduce(acc, p);
+    o[1] = acc;
+  } else if (d.cls == 1) {
+    o[0] = Pa;
+    rot_acc(acc, Pa, d.x, p);
+    reduce(acc, p);
+    o[1] = acc;
+  } else if (d.cls == 2) {
+    reduce(acc, p);
+    o[0] = acc;
+    o[1] = Pa;
+    wxor(o[1], o[0]);
+  } else if (d.cls == 3) {
+    wxor(acc, Pa);
+    reduce(acc, p);
+    const Word<NL> t = acc;
+    Word<NL> S = t;
+    const int M = (p + 1) / 2;
+    const int bz = (2 * (d.y - d.x)) % p;
+    const int top = 31 - __clz(M);
+    int m = 1;
+#pragma unroll 1
+    for (int bit = top - 1; bit >= 0; bit--) {
+      Word<NL> nx = S;
+      rot_acc(nx, S, (bz * m) % p, p);
+      reduce(nx, p);
+      S = nx;
+      m *= 2;
+      if ((M >> bit) & 1) {
+        nx = S;
+        rot_acc(nx, t, (bz * m) % p, p);
+        reduce(nx, p);
+        S = nx;
+        m += 1;
+      }
+    }
+    o[1] = S;
+    o[0] = S;
+    wxor(o[0], Pa);
+  } else if (d.cls == 4) {  // scrub: syndromes of both parity equations
+    reduce(acc, p);
+    wxor(acc, Pa);
+    uint32_t nz = 0;
+#pragma unroll
+    for (int j = 0; j < NL; j++) nz |= acc.v[j] | Pa.v[j];
+    bad += valid && nz;
+  } else {  // update
+    o[0] = Pa;
+    reduce(acc, p);
+    o[1] = acc;
+    o[2] = NEWW;
+  }
+}
+
+template <int P, int WI>
+struct GroupWords {  // compile-time loop over the group's words
+  template <class F>
+  __device__ __forceinline__ static void run(F&& f) {
+    if constexpr (WI < GP<P>::g) {
+      f(std::integral_constant<int, WI>{});
+      GroupWords<P, WI + 1>::run(f);
+    }
+  }
+};
+
+template <int P>
+__global__ void __launch_bounds__(128) zp_generic_kernel(const __grid_constant__ ZpArgs a, int mode) {
+  using GG = GP<P>;
+  constexpr int n = GG::n, NL = GG::NL, g = GG::g, GB = GG::GB, W4 = GG::W4;
   const uint64_t W = (8 * a.bytes + n - 1) / n;
   uint64_t g0, g1;
-  group_span(a, mode, n, g, gbytes, g0, g1);
+  group_span(a, mode, n, g, GB, g0, g1);
   const uint64_t groups = g1 - g0;
   const uint64_t total = groups * static_cast<uint64_t>(a.num_stripes);
   for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
        u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int s = static_cast<int>(u / groups);
     const uint64_t grp = g0 + (u - static_cast<uint64_t>(s) * groups);
-    const Desc d = desc_of(a, s, mode, p);
-    const bool ext = a.N > p;
+    const uint64_t byte0 = grp * static_cast<uint64_t>(GB);
+    const Desc d = desc_of(a, s, mode, P);
+    const bool ext = a.N > P;
     // rows: partial = this rank's surviving strips [k_lo, k_hi); combine = nsrc partial slots
     int R = mode == KMODE_SCRUB ? a.N + 2 : (mode == KMODE_UPDATE ? a.upd_rows : a.N);
     if (mode == KMODE_PARTIAL)
       R = a.k_hi - a.k_lo - (d.x >= a.k_lo && d.x < a.k_hi) - (d.y >= a.k_lo && d.y < a.k_hi);
     if (mode == KMODE_COMBINE) R = a.nsrc;
+    Word<NL> Pa[g], acc[g], NEWW[g];
+#pragma unroll
+    for (int wi = 0; wi < g; wi++) {
+      wzero(Pa[wi]);
+      wzero(acc[wi]);
+      wzero(NEWW[wi]);
+    }
+    uint32_t buf[W4 + 1];
+    for (int r = 0; r < R; r++) {
+      if (mode == KMODE_COMBINE) {  // partial slots hold reduced words of bytes [range_lo, ...)
+        const uint64_t so = static_cast<uint64_t>(s) * a.part_stride;
+        const uint64_t off = byte0 - a.range_lo, ll = a.pbytes - a.range_lo;
+        load_group<W4>(a.src_p[r] + so, ll, off, buf);
+        GroupWords<P, 0>::run([&](auto wc) {
+          Word<NL> L;
+          group_word<P, decltype(wc)::value>(buf, L);
+          wxor(Pa[decltype(wc)::value], L);
+        });
+        load_group<W4>(a.src_q[r] + so, ll, off, buf);
+        GroupWords<P, 0>::run([&](auto wc) {
+          Word<NL> L;
+          group_word<P, decltype(wc)::value>(buf, L);
+          wxor(acc[decltype(wc)::value], L);
+        });
+        continue;
+      }
+      int k;
+      if (mode == KMODE_SCRUB) k = r;
+      else if (mode == KMODE_UPDATE) k = r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
+      else {
+        k = mode == KMODE_PARTIAL ? a.k_lo + r : r;
+        const int lo = mode == KMODE_PARTIAL ? a.k_lo : 0;
+        if (d.x >= lo && k >= d.x) k++;
+        if (d.y >= lo && k >= d.y) k++;
+      }
+      load_group<W4>(rptr(a, k, s), rlen(a, k), byte0, buf);
+      const bool is_new = k == K_NEW;
+      if (is_new) k = d.x;
+      int amt = 0;
+      if (!(ext && k < a.N)) {
+        amt = ((k < a.N ? k : P) - d.base) % P;
+        if (amt < 0) amt += P;
+      }
+      GroupWords<P, 0>::run([&](auto wc) {
+        constexpr int WI = decltype(wc)::value;
+        Word<NL> L;
+        group_word<P, WI>(buf, L);
+        if (is_new) NEWW[WI] = L;
+        if (k <= a.N) wxor(Pa[WI], L);
+        if (k != a.N) {
+          if (ext && k < a.N) add_coeff(acc[WI], L, k, P);
+          else rot_acc(acc[WI], L, amt, P);
+        }
+      });
+    }
     int kout[3] = {0, 0, 0};
     int nout = 2;
     if (d.cls == 0) { kout[0] = a.N; kout[1] = a.N + 1; }
@@ -247,135 +446,27 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
     else if (d.cls == 3) { kout[0] = d.x; kout[1] = d.y; }
     else if (d.cls == 4) { nout = 0; }
     else { kout[0] = a.N; kout[1] = a.N + 1; kout[2] = d.x; nout = 3; }
-    uint32_t ob[3][GROUP_MAX_WORDS32];
-    for (int q = 0; q < nout; q++)
-      for (int i = 0; i <= glimbs; i++) ob[q][i] = 0;
-    uint32_t bad = 0;
-    for (int wi = 0; wi < g; wi++) {
-      const uint64_t w = grp * g + wi;
-      Word<NL> Pa, acc, L, NEWW, o[3];
-      wzero(Pa);
-      wzero(acc);
-      wzero(NEWW);
-      for (int r = 0; r < R; r++) {
-        if (mode == KMODE_COMBINE) {  // partial slots hold reduced words of bytes [range_lo, ...)
-          const uint64_t so = static_cast<uint64_t>(s) * a.part_stride;
-          const uint64_t wl = w - (a.range_lo * 8) / n, ll = a.pbytes - a.range_lo;
-          load_word(a.src_p[r] + so, ll, wl, n, L);
-          wxor(Pa, L);
-          load_word(a.src_q[r] + so, ll, wl, n, L);
-          wxor(acc, L);
-          continue;
-        }
-        int k;
-        if (mode == KMODE_SCRUB) k = r;
-        else if (mode == KMODE_UPDATE) k = r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
-        else {
-          k = mode == KMODE_PARTIAL ? a.k_lo + r : r;
-          const int lo = mode == KMODE_PARTIAL ? a.k_lo : 0;
-          if (d.x >= lo && k >= d.x) k++;
-          if (d.y >= lo && k >= d.y) k++;
-        }
-        load_word(rptr(a, k, s), rlen(a, k), w, n, L);
-        if (k == K_NEW) {
-          NEWW = L;
-          k = d.x;
-        }
-        if (k <= a.N) wxor(Pa, L);
-        if (k != a.N) {
-          if (ext && k < a.N) {
-            add_coeff(acc, L, k, p);
-          } else {
-            int amt = ((k < a.N ? k : p) - d.base) % p;
-            if (amt < 0) amt += p;
-            rot_acc(acc, L, amt, p);
-          }
-        }
-      }
-      const ExtProg* pr = ext ? a.prog + pair_index(d.x, d.y, a.N) : nullptr;
-      if (mode == KMODE_PARTIAL) {  // unsolved partial syndromes (NEXT-4)
-        o[0] = Pa;
-        reduce(acc, p);
-        o[1] = acc;
-      } else if (ext && (d.cls == 1 || d.cls == 2 || d.cls == 3)) {  // extended code (Lemma 23.2 with Eq. (qext))
-        if (d.cls == 1) {
-          o[0] = Pa;
-          add_coeff(acc, Pa, d.x, p);
-          reduce(acc, p);
-          o[1] = acc;
-        } else if (d.cls == 2) {
-          reduce(acc, p);
-          mul_prog(acc, pr, p, o[0]);
-          o[1] = Pa;
-          wxor(o[1], o[0]);
-        } else {
-          add_coeff(acc, Pa, d.x, p);
-          reduce(acc, p);
-          mul_prog(acc, pr, p, o[1]);
-          o[0] = o[1];
-          wxor(o[0], Pa);
-        }
-      } else if (d.cls == 0) {
-        o[0] = Pa;
-        reduce(acc, p);
-        o[1] = acc;
-      } else if (d.cls == 1) {
-        o[0] = Pa;
-        rot_acc(acc, Pa, d.x, p);
-        reduce(acc, p);
-        o[1] = acc;
-      } else if (d.cls == 2) {
-        reduce(acc, p);
-        o[0] = acc;
-        o[1] = Pa;
-        wxor(o[1], o[0]);
-      } else if (d.cls == 3) {
-        wxor(acc, Pa);
-        reduce(acc, p);
-        const Word<NL> t = acc;
-        Word<NL> S = t;
-        const int M = (p + 1) / 2;
-        const int bz = (2 * (d.y - d.x)) % p;
-        int top = 31 - __clz(M);
-        int m = 1;
-        for (int bit = top - 1; bit >= 0; bit--) {
-          Word<NL> nx = S;
-          rot_acc(nx, S, (bz * m) % p, p);
-          reduce(nx, p);
-          S = nx;
-          m *= 2;
-          if ((M >> bit) & 1) {
-            nx = S;
-            rot_acc(nx, t, (bz * m) % p, p);
-            reduce(nx, p);
-            S = nx;
-            m += 1;
-          }
-        }
-        o[1] = S;
-        o[0] = S;
-        wxor(o[0], Pa);
-      } else if (d.cls == 4) {  // scrub: syndromes of both parity equations
-        reduce(acc, p);
-        wxor(acc, Pa);
-        uint32_t nz = 0;
+    uint32_t ob[3][W4 + 1];
 #pragma unroll
-        for (int j = 0; j < NL; j++) nz |= acc.v[j] | Pa.v[j];
-        bad += (w < W) && nz;
-      } else {  // update
-        o[0] = Pa;
-        reduce(acc, p);
-        o[1] = acc;
-        o[2] = NEWW;
-      }
-      for (int q = 0; q < nout; q++) put_word(ob[q], o[q], wi * n, n);
-    }
+    for (int q = 0; q < 3; q++)
+#pragma unroll
+      for (int i = 0; i <= W4; i++) ob[q][i] = 0;
+    uint32_t bad = 0;
+    GroupWords<P, 0>::run([&](auto wc) {
+      constexpr int WI = decltype(wc)::value;
+      Word<NL> o[3];
+      finish_word<NL>(a, d, P, mode, ext, Pa[WI], acc[WI], NEWW[WI], o, grp * g + WI < W, bad);
+#pragma unroll
+      for (int q = 0; q < 3; q++)
+        if (q < nout) group_put<P, WI>(ob[q], o[q]);
+    });
     if (mode == KMODE_SCRUB) {
       if (bad) atomicAdd(a.counts + s, bad);
       continue;
     }
-    const uint64_t byte0 = grp * static_cast<uint64_t>(gbytes);
-    for (int q = 0; q < nout; q++) {
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+      if (q >= nout) break;
       uint8_t* gq;  // address of byte byte0 of output q
       uint64_t left;
       if (mode == KMODE_PARTIAL) {  // slot of the owner of this word range
@@ -388,27 +479,19 @@ __global__ void zp_generic_kernel(const __grid_constant__ ZpArgs a, int p, int m
         const uint64_t len = rlen(a, kout[q]);
         left = len > byte0 ? len - byte0 : 0;
       }
-      const int nb = static_cast<int>(left < static_cast<uint64_t>(gbytes) ? left : gbytes);
-      if ((reinterpret_cast<uintptr_t>(gq) & 3u) == 0 && nb == gbytes && (gbytes & 3) == 0) {
-        for (int i = 0; i < glimbs; i++) reinterpret_cast<uint32_t*>(gq)[i] = ob[q][i];
-      } else {
-        for (int i = 0; i < nb; i++) gq[i] = static_cast<uint8_t>(ob[q][i >> 2] >> (8 * (i & 3)));
-      }
+      const int nb = static_cast<int>(left < static_cast<uint64_t>(GB) ? left : GB);
+      store_group<W4>(gq, nb, ob[q]);
     }
   }
 }
 
-}  // namespace
-
-cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, int num_sms) {
-  const int n = p - 1;
-  const int g = 8 / (n & 7 ? ((n & 3) ? 2 : 4) : 8);
-  const int gbytes = g * n / 8;
-  const uint64_t W = (8 * a.bytes + n - 1) / n;
-  uint64_t g0 = 0, g1 = (W + g - 1) / g;
+template <int P>
+cudaError_t launch_p(const ZpArgs& a, int mode, cudaStream_t st, int num_sms) {
+  using GG = GP<P>;
+  uint64_t g0 = 0, g1 = ((8 * a.bytes + GG::n - 1) / GG::n + GG::g - 1) / GG::g;
   if (mode == KMODE_COMBINE) {
-    g0 = a.range_lo / gbytes;
-    g1 = std::min<uint64_t>(g1, (a.range_hi + gbytes - 1) / gbytes);
+    g0 = a.range_lo / GG::GB;
+    g1 = std::min<uint64_t>(g1, (a.range_hi + GG::GB - 1) / GG::GB);
     if (g1 < g0) g1 = g0;
   }
   const uint64_t total = (g1 - g0) * static_cast<uint64_t>(a.num_stripes);
@@ -417,19 +500,27 @@ cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, in
   const uint64_t cap = static_cast<uint64_t>(num_sms) * 16;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
-  const dim3 grid(static_cast<unsigned>(blocks));
-  switch ((p + 31) / 32) {  // 32-bit limbs per p-bit slot
-    case 1: zp_generic_kernel<1><<<grid, threads, 0, st>>>(a, p, mode); break;
-    case 2: zp_generic_kernel<2><<<grid, threads, 0, st>>>(a, p, mode); break;
-    case 3: zp_generic_kernel<3><<<grid, threads, 0, st>>>(a, p, mode); break;
-    case 4: zp_generic_kernel<4><<<grid, threads, 0, st>>>(a, p, mode); break;
-    case 5: zp_generic_kernel<5><<<grid, threads, 0, st>>>(a, p, mode); break;
-    case 6: zp_generic_kernel<6><<<grid, threads, 0, st>>>(a, p, mode); break;
-    case 7: zp_generic_kernel<7><<<grid, threads, 0, st>>>(a, p, mode); break;
-    case 8: zp_generic_kernel<8><<<grid, threads, 0, st>>>(a, p, mode); break;
-    default: zp_generic_kernel<9><<<grid, threads, 0, st>>>(a, p, mode); break;
-  }
+  zp_generic_kernel<P><<<dim3(static_cast<unsigned>(blocks)), threads, 0, st>>>(a, mode);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+// The 26 primes whose period lcm(p-1, 32) exceeds 32 lanes, plus the fast primes without
+// extended-code kernels (3, 7, 31, 73: Theorem 25.3 fails, so never reached by a valid plan).
+cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, int num_sms) {
+  switch (p) {
+#define ZP_GEN_CASE(PP) \
+  case PP: return launch_p<PP>(a, mode, st, num_sms);
+    ZP_GEN_CASE(3) ZP_GEN_CASE(7) ZP_GEN_CASE(31) ZP_GEN_CASE(73)
+    ZP_GEN_CASE(67) ZP_GEN_CASE(71) ZP_GEN_CASE(79) ZP_GEN_CASE(83) ZP_GEN_CASE(103) ZP_GEN_CASE(107)
+    ZP_GEN_CASE(127) ZP_GEN_CASE(131) ZP_GEN_CASE(139) ZP_GEN_CASE(149) ZP_GEN_CASE(151) ZP_GEN_CASE(157)
+    ZP_GEN_CASE(163) ZP_GEN_CASE(167) ZP_GEN_CASE(173) ZP_GEN_CASE(179) ZP_GEN_CASE(181) ZP_GEN_CASE(191)
+    ZP_GEN_CASE(197) ZP_GEN_CASE(199) ZP_GEN_CASE(211) ZP_GEN_CASE(223) ZP_GEN_CASE(227) ZP_GEN_CASE(229)
+    ZP_GEN_CASE(239) ZP_GEN_CASE(251)
+#undef ZP_GEN_CASE
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 }  // namespace zp
