@@ -1,517 +1,47 @@
-// zp_generic.cu -- Z_p-RAID kernel for the primes without a fast (TMA) specialisation
-// (zp_fast.cuh needs a period lcm(p-1, 32) of at most 32 lanes; the other 26 odd primes <= 257
-// run here).  Same mathematics, simpler mapping:
-//   * one thread per byte-aligned group of g = 8/gcd(n,8) words (GB = g*n/8 bytes, so outputs
-//     are whole bytes and no two threads touch the same byte); p is a template parameter, so
-//     the group geometry, every word's bit offset and the limb count NL = ceil(p/32) are
-//     compile-time;
-//   * per strip, the group's GB bytes are read with aligned 32-bit loads (realigned by one
-//     funnel shift) and the g words are cut out at compile-time offsets; each word is held as
-//     a p-bit value in NL 32-bit limbs (slot bit p-1 = the R' overflow); multiplication by x^a
-//     is a rotation of the p-bit slot done limb-wise (a funnel-shift stage plus a log2(NL)-step
-//     limb barrel shifter with static register indexing); the reduction pi is deferred to the
-//     end of each sum;
-//   * the class epilogues are the same as the fast path (Lemma 23.2 proof PAPER.md:380-401,
-//     Sec. 4.6), the DD inverse by the same doubling chain; outputs are
-//     packed at compile-time offsets and written with aligned 32-bit stores (byte stores only
-//     at the group's edges).
-// No TMA and no shared memory.
-#include <algorithm>
-#include <cstdint>
-#include <type_traits>
-#include <cuda_runtime.h>
-
-#include "zp_args.h"
+// zp_generic.cu -- dispatch of the generic kernel (zp_generic.cuh) by p; the instantiations
+// live in zp_generic_{a,b,c}.cu.
+#include "zp_generic.cuh"
 
 namespace zp {
-namespace {
-
-template <int NL>
-struct Word {
-  uint32_t v[NL];
-};
-
-template <int NL>
-__device__ __forceinline__ void wzero(Word<NL>& w) {
-#pragma unroll
-  for (int i = 0; i < NL; i++) w.v[i] = 0;
-}
-template <int NL>
-__device__ __forceinline__ void wxor(Word<NL>& a, const Word<NL>& b) {
-#pragma unroll
-  for (int i = 0; i < NL; i++) a.v[i] ^= b.v[i];
-}
-// Mask of the low `bits` bits, limb i.
-__device__ __forceinline__ uint32_t low_mask(int bits, int i) {
-  const int r = bits - 32 * i;
-  return r >= 32 ? 0xFFFFFFFFu : (r <= 0 ? 0u : ((1u << r) - 1u));
-}
-
-// out = in << s (s < 32*NL), bits beyond 32*NL dropped.
-template <int NL>
-__device__ __forceinline__ void shl(const Word<NL>& in, int s, Word<NL>& t) {
-  const uint32_t r = static_cast<uint32_t>(s & 31);
-  const int q = s >> 5;
-#pragma unroll
-  for (int i = NL - 1; i >= 0; i--) t.v[i] = __funnelshift_l(i > 0 ? in.v[i - 1] : 0u, in.v[i], r);
-#pragma unroll
-  for (int b = 1; b < NL; b <<= 1)
-    if (q & b) {
-#pragma unroll
-      for (int i = NL - 1; i >= 0; i--) t.v[i] = i >= b ? t.v[i - b] : 0u;
-    }
-}
-// out = in >> s (s < 32*NL).
-template <int NL>
-__device__ __forceinline__ void shr(const Word<NL>& in, int s, Word<NL>& t) {
-  const uint32_t r = static_cast<uint32_t>(s & 31);
-  const int q = s >> 5;
-#pragma unroll
-  for (int i = 0; i < NL; i++) t.v[i] = __funnelshift_r(in.v[i], i + 1 < NL ? in.v[i + 1] : 0u, r);
-#pragma unroll
-  for (int b = 1; b < NL; b <<= 1)
-    if (q & b) {
-#pragma unroll
-      for (int i = 0; i < NL; i++) t.v[i] = i + b < NL ? t.v[i + b] : 0u;
-    }
-}
-
-// acc ^= rot_a(src) inside the p-bit slot (src has slot bit p-1 clear; a in [0, p)):
-// x^a * src in R' = F2[x]/(x^p + 1) (Eq. (powers)).
-template <int NL>
-__device__ __forceinline__ void rot_acc(Word<NL>& acc, const Word<NL>& src, int a, int p) {
-  if (a == 0) {
-    wxor(acc, src);
-    return;
-  }
-  Word<NL> l, r;
-  shl(src, a, l);
-  shr(src, p - a, r);
-#pragma unroll
-  for (int i = 0; i < NL; i++) acc.v[i] ^= (l.v[i] | r.v[i]) & low_mask(p, i);
-}
-
-// pi: if slot bit p-1 is set, flip bits 0..n-1 and clear bit p-1.
-template <int NL>
-__device__ __forceinline__ void reduce(Word<NL>& w, int p) {
-  const int n = p - 1;
-  uint32_t t = 0;
-#pragma unroll
-  for (int i = 0; i < NL; i++)
-    if (i == (n >> 5)) t = (w.v[i] >> (n & 31)) & 1u;  // (static register indexing)
-  const uint32_t f = 0u - t;
-#pragma unroll
-  for (int i = 0; i < NL; i++) w.v[i] = (w.v[i] ^ (f & low_mask(n, i))) & low_mask(n, i);
-}
-
-struct Desc {
-  int x, y, cls, base;  // cls: 0 PQ, 1 DQ, 2 DP, 3 DD, 4 scrub, 5 update (x = rewritten strip)
-};
-
-__device__ Desc desc_of(const ZpArgs& a, int s, int mode, int p) {
-  Desc d;
-  if (mode == KMODE_SCRUB) {
-    d.x = d.y = -1; d.cls = 4; d.base = 0;
-    return d;
-  }
-  if (mode == KMODE_UPDATE) {
-    d.x = a.upd ? a.upd[static_cast<int64_t>(s) * a.upd_stride] : a.upd_k;
-    d.y = -1; d.cls = 5; d.base = 0;
-    return d;
-  }
-  int i = a.N, j = a.N + 1;
-  if (mode == KMODE_RECOVER || mode == KMODE_PARTIAL || mode == KMODE_COMBINE) {
-    if (a.er) {
-      const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
-      i = e.x; j = e.y;
-    } else {
-      i = a.ei; j = a.ej;
-    }
-  }
-  d.x = i < j ? i : j;
-  d.y = i < j ? j : i;
-  if (d.y == a.N + 1) d.cls = (d.x == a.N) ? 0 : 1;  // PQ : DQ
-  else d.cls = (d.y == a.N) ? 2 : 3;                  // DP : DD
-  // basic code: rotation origin at the lost strip; extended code (N > p): origin 0 + ExtProg
-  d.base = (a.N <= p && (d.cls == 2 || d.cls == 3)) ? d.x : 0;
-  return d;
-}
-
-// acc ^= g_k * v with g_k the Eq. (qext) coefficient of data strip k (x^k, or 1 + x^{k-p+1}).
-template <int NL>
-__device__ __forceinline__ void add_coeff(Word<NL>& acc, const Word<NL>& v, int k, int p) {
-  if (k < p) {
-    rot_acc(acc, v, k, p);
-  } else {
-    rot_acc(acc, v, 0, p);
-    rot_acc(acc, v, k - p + 1, p);
-  }
-}
-
-// out = u * t for the pair's ExtProg: u = sum_i x^{e_i}, or, for a geometric pair,
-// u = x^{e0} sum_{m<(p+1)/2} x^{bz m} (= x^{e0} (1 + x^{bz/2})^{-1}, reading R11).
-template <int NL>
-__device__ void mul_prog(const Word<NL>& t, const ExtProg* pr, int p, Word<NL>& out) {
-  wzero(out);
-  if (pr->geo_bz) {
-    for (int m = 0; m < (p + 1) / 2; m++) rot_acc(out, t, (pr->geo_bz * m + pr->geo_e0) % p, p);
-  } else {
-    for (int i = 0; i < pr->nu; i++) rot_acc(out, t, pr->e[i], p);
-  }
-  reduce(out, p);
-}
-
-__device__ __forceinline__ uint64_t sstride(const ZpArgs& a, int k) { return k < a.N ? a.data_stride : a.parity_stride; }
-constexpr int K_NEW = -1;
-__device__ __forceinline__ const uint8_t* rptr(const ZpArgs& a, int k, int s) {
-  return k == K_NEW ? a.nbase + static_cast<uint64_t>(s) * a.new_stride : a.base[k] + static_cast<uint64_t>(s) * sstride(a, k);
-}
-__device__ __forceinline__ uint64_t rlen(const ZpArgs& a, int k) {
-  return (k == K_NEW || k < a.N) ? a.bytes : a.pbytes;
-}
-
-// Compile-time group geometry of prime P.
-template <int P>
-struct GP {
-  static constexpr int n = P - 1;
-  static constexpr int NL = (P + 31) / 32;                                  // limbs per p-bit slot
-  static constexpr int g = 8 / ((n & 7) == 0 ? 8 : ((n & 3) == 0 ? 4 : 2));  // words per group
-  static constexpr int GB = g * n / 8;                                      // bytes per group
-  static constexpr int W4 = (GB + 3) / 4;                                   // 32-bit words per group
-};
-
-// Group range of one launch: all groups of the strip, or (combine) the groups of bytes
-// [range_lo, range_hi) -- range_lo is a multiple of the group size (host-checked).
-__device__ __forceinline__ void group_span(const ZpArgs& a, int mode, int n, int g, int gbytes, uint64_t& g0,
-                                           uint64_t& g1) {
-  const uint64_t W = (8 * a.bytes + n - 1) / n;
-  const uint64_t groups = (W + g - 1) / g;
-  g0 = 0;
-  g1 = groups;
-  if (mode == KMODE_COMBINE) {
-    g0 = a.range_lo / gbytes;
-    const uint64_t e = (a.range_hi + gbytes - 1) / gbytes;
-    g1 = e < groups ? e : groups;
-    if (g1 < g0) g1 = g0;
-  }
-}
-
-// buf[0..W4) = bytes [byte0, byte0 + 4*W4) of a row of `len` bytes, zero past `len`
-// (reading R5's zero extension); buf[W4] = 0.
-template <int W4>
-__device__ __forceinline__ void load_group(const uint8_t* row, uint64_t len, uint64_t byte0, uint32_t (&buf)[W4 + 1]) {
-  const uint8_t* pg = row + byte0;
-  const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(pg) & 3u);
-  buf[W4] = 0u;
-  if (byte0 + 4 * W4 + 4 <= len + mis) {  // the aligned words [pg - mis, pg - mis + 4(W4+1)) lie in the row
-    const uint32_t* q = reinterpret_cast<const uint32_t*>(pg - mis);
-    uint32_t raw[W4 + 1];
-#pragma unroll
-    for (int i = 0; i <= W4; i++) raw[i] = __ldg(q + i);
-#pragma unroll
-    for (int i = 0; i < W4; i++) buf[i] = __funnelshift_r(raw[i], raw[i + 1], 8 * mis);
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < W4; i++) {
-    uint32_t v = 0;
-#pragma unroll
-    for (int b = 0; b < 4; b++)
-      if (byte0 + 4 * i + b < len) v |= static_cast<uint32_t>(__ldg(pg + 4 * i + b)) << (8 * b);
-    buf[i] = v;
-  }
-}
-
-// Word WI of the group (bits [WI*n, WI*n + n) of buf), compile-time offsets.
-template <int P, int WI>
-__device__ __forceinline__ void group_word(const uint32_t (&buf)[GP<P>::W4 + 1], Word<GP<P>::NL>& out) {
-  constexpr int n = GP<P>::n;
-#pragma unroll
-  for (int i = 0; i < GP<P>::NL; i++) {
-    const int pos = WI * n + 32 * i, idx = pos >> 5, sh = pos & 31;
-    const uint32_t lo = idx < GP<P>::W4 + 1 ? buf[idx < GP<P>::W4 + 1 ? idx : 0] : 0u;
-    const uint32_t hi = idx + 1 < GP<P>::W4 + 1 ? buf[idx + 1 < GP<P>::W4 + 1 ? idx + 1 : 0] : 0u;
-    out.v[i] = 32 * i < n ? (__funnelshift_r(lo, hi, sh) & low_mask(n, i)) : 0u;
-  }
-}
-
-// ob |= word v at bit offset WI*n (compile-time).
-template <int P, int WI>
-__device__ __forceinline__ void group_put(uint32_t (&ob)[GP<P>::W4 + 1], const Word<GP<P>::NL>& v) {
-  constexpr int n = GP<P>::n;
-#pragma unroll
-  for (int i = 0; i < GP<P>::NL; i++) {
-    if (32 * i >= n) break;
-    const int pos = WI * n + 32 * i, idx = pos >> 5, sh = pos & 31;
-    if (idx < GP<P>::W4 + 1) ob[idx < GP<P>::W4 + 1 ? idx : 0] |= v.v[i] << sh;
-    if (sh && idx + 1 < GP<P>::W4 + 1) ob[idx + 1 < GP<P>::W4 + 1 ? idx + 1 : 0] |= v.v[i] >> (32 - sh);
-  }
-}
-
-// Bytes [0, nb) of the group buffer to dst: aligned 32-bit stores, byte stores at the edges.
-template <int W4>
-__device__ __forceinline__ void store_group(uint8_t* dst, int nb, const uint32_t (&ob)[W4 + 1]) {
-  const uint32_t mis = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst) & 3u);
-  uint32_t* q = reinterpret_cast<uint32_t*>(dst - mis);
-#pragma unroll
-  for (int j = 0; j <= W4; j++) {  // word j of q holds group bytes [4j - mis, 4j - mis + 4)
-    const uint32_t v = __funnelshift_l(j > 0 ? ob[j > 0 ? j - 1 : 0] : 0u, ob[j], 8 * mis);
-    const int b0 = 4 * j - static_cast<int>(mis);
-    if (b0 >= 0 && b0 + 4 <= nb) {
-      q[j] = v;
-    } else {
-#pragma unroll
-      for (int b = 0; b < 4; b++)
-        if (b0 + b >= 0 && b0 + b < nb) dst[b0 + b] = static_cast<uint8_t>(v >> (8 * b));
-    }
-  }
-}
-
-// Class epilogue of one word: o[0..nout) from the folded Pa / acc (and NEWW for the update).
-template <int NL>
-__device__ __forceinline__ void finish_word(const ZpArgs& a, const Desc& d, int p, int mode, bool ext, Word<NL>& Pa,
-                                            Word<NL>& acc, const Word<NL>& NEWW, Word<NL> (&o)[3], bool valid,
-                                            uint32_t& bad) {
-  const ExtProg* pr = ext ? a.prog + pair_index(d.x, d.y, a.N) : nullptr;
-  if (mode == KMODE_PARTIAL) {  // unsolved partial syndromes (NEXT-4)
-    o[0] = Pa;
-    reduce(acc, p);
-    o[1] = acc;
-  } else if (ext && (d.cls == 1 || d.cls == 2 || d.cls == 3)) {  // extended code (Lemma 23.2 with Eq. (qext))
-    if (d.cls == 1) {
-      o[0] = Pa;
-      add_coeff(acc, Pa, d.x, p);
-      reduce(acc, p);
-      o[1] = acc;
-    } else if (d.cls == 2) {
-      reduce(acc, p);
-      mul_prog(acc, pr, p, o[0]);
-      o[1] = Pa;
-      wxor(o[1], o[0]);
-    } else {
-      add_coeff(acc, Pa, d.x, p);
-      reduce(acc, p);
-      mul_prog(acc, pr, p, o[1]);
-      o[0] = o[1];
-      wxor(o[0], Pa);
-    }
-  } else if (d.cls == 0) {
-    o[0] = Pa;
-    reduce(acc, p);
-    o[1] = acc;
-  } else if (d.cls == 1) {
-    o[0] = Pa;
-    rot_acc(acc, Pa, d.x, p);
-    reduce(acc, p);
-    o[1] = acc;
-  } else if (d.cls == 2) {
-    reduce(acc, p);
-    o[0] = acc;
-    o[1] = Pa;
-    wxor(o[1], o[0]);
-  } else if (d.cls == 3) {
-    wxor(acc, Pa);
-    reduce(acc, p);
-    const Word<NL> t = acc;
-    Word<NL> S = t;
-    const int M = (p + 1) / 2;
-    const int bz = (2 * (d.y - d.x)) % p;
-    const int top = 31 - __clz(M);
-    int m = 1;
-#pragma unroll 1
-    for (int bit = top - 1; bit >= 0; bit--) {
-      Word<NL> nx = S;
-      rot_acc(nx, S, (bz * m) % p, p);
-      reduce(nx, p);
-      S = nx;
-      m *= 2;
-      if ((M >> bit) & 1) {
-        nx = S;
-        rot_acc(nx, t, (bz * m) % p, p);
-        reduce(nx, p);
-        S = nx;
-        m += 1;
-      }
-    }
-    o[1] = S;
-    o[0] = S;
-    wxor(o[0], Pa);
-  } else if (d.cls == 4) {  // scrub: syndromes of both parity equations
-    reduce(acc, p);
-    wxor(acc, Pa);
-    uint32_t nz = 0;
-#pragma unroll
-    for (int j = 0; j < NL; j++) nz |= acc.v[j] | Pa.v[j];
-    bad += valid && nz;
-  } else {  // update
-    o[0] = Pa;
-    reduce(acc, p);
-    o[1] = acc;
-    o[2] = NEWW;
-  }
-}
-
-template <int P, int WI>
-struct GroupWords {  // compile-time loop over the group's words
-  template <class F>
-  __device__ __forceinline__ static void run(F&& f) {
-    if constexpr (WI < GP<P>::g) {
-      f(std::integral_constant<int, WI>{});
-      GroupWords<P, WI + 1>::run(f);
-    }
-  }
-};
-
-template <int P>
-__global__ void __launch_bounds__(128) zp_generic_kernel(const __grid_constant__ ZpArgs a, int mode) {
-  using GG = GP<P>;
-  constexpr int n = GG::n, NL = GG::NL, g = GG::g, GB = GG::GB, W4 = GG::W4;
-  const uint64_t W = (8 * a.bytes + n - 1) / n;
-  uint64_t g0, g1;
-  group_span(a, mode, n, g, GB, g0, g1);
-  const uint64_t groups = g1 - g0;
-  const uint64_t total = groups * static_cast<uint64_t>(a.num_stripes);
-  for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
-       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const int s = static_cast<int>(u / groups);
-    const uint64_t grp = g0 + (u - static_cast<uint64_t>(s) * groups);
-    const uint64_t byte0 = grp * static_cast<uint64_t>(GB);
-    const Desc d = desc_of(a, s, mode, P);
-    const bool ext = a.N > P;
-    // rows: partial = this rank's surviving strips [k_lo, k_hi); combine = nsrc partial slots
-    int R = mode == KMODE_SCRUB ? a.N + 2 : (mode == KMODE_UPDATE ? a.upd_rows : a.N);
-    if (mode == KMODE_PARTIAL)
-      R = a.k_hi - a.k_lo - (d.x >= a.k_lo && d.x < a.k_hi) - (d.y >= a.k_lo && d.y < a.k_hi);
-    if (mode == KMODE_COMBINE) R = a.nsrc;
-    Word<NL> Pa[g], acc[g], NEWW[g];
-#pragma unroll
-    for (int wi = 0; wi < g; wi++) {
-      wzero(Pa[wi]);
-      wzero(acc[wi]);
-      wzero(NEWW[wi]);
-    }
-    uint32_t buf[W4 + 1];
-    for (int r = 0; r < R; r++) {
-      if (mode == KMODE_COMBINE) {  // partial slots hold reduced words of bytes [range_lo, ...)
-        const uint64_t so = static_cast<uint64_t>(s) * a.part_stride;
-        const uint64_t off = byte0 - a.range_lo, ll = a.pbytes - a.range_lo;
-        load_group<W4>(a.src_p[r] + so, ll, off, buf);
-        GroupWords<P, 0>::run([&](auto wc) {
-          Word<NL> L;
-          group_word<P, decltype(wc)::value>(buf, L);
-          wxor(Pa[decltype(wc)::value], L);
-        });
-        load_group<W4>(a.src_q[r] + so, ll, off, buf);
-        GroupWords<P, 0>::run([&](auto wc) {
-          Word<NL> L;
-          group_word<P, decltype(wc)::value>(buf, L);
-          wxor(acc[decltype(wc)::value], L);
-        });
-        continue;
-      }
-      int k;
-      if (mode == KMODE_SCRUB) k = r;
-      else if (mode == KMODE_UPDATE) k = r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
-      else {
-        k = mode == KMODE_PARTIAL ? a.k_lo + r : r;
-        const int lo = mode == KMODE_PARTIAL ? a.k_lo : 0;
-        if (d.x >= lo && k >= d.x) k++;
-        if (d.y >= lo && k >= d.y) k++;
-      }
-      load_group<W4>(rptr(a, k, s), rlen(a, k), byte0, buf);
-      const bool is_new = k == K_NEW;
-      if (is_new) k = d.x;
-      int amt = 0;
-      if (!(ext && k < a.N)) {
-        amt = ((k < a.N ? k : P) - d.base) % P;
-        if (amt < 0) amt += P;
-      }
-      GroupWords<P, 0>::run([&](auto wc) {
-        constexpr int WI = decltype(wc)::value;
-        Word<NL> L;
-        group_word<P, WI>(buf, L);
-        if (is_new) NEWW[WI] = L;
-        if (k <= a.N) wxor(Pa[WI], L);
-        if (k != a.N) {
-          if (ext && k < a.N) add_coeff(acc[WI], L, k, P);
-          else rot_acc(acc[WI], L, amt, P);
-        }
-      });
-    }
-    int kout[3] = {0, 0, 0};
-    int nout = 2;
-    if (d.cls == 0) { kout[0] = a.N; kout[1] = a.N + 1; }
-    else if (d.cls == 1) { kout[0] = d.x; kout[1] = a.N + 1; }
-    else if (d.cls == 2) { kout[0] = d.x; kout[1] = a.N; }
-    else if (d.cls == 3) { kout[0] = d.x; kout[1] = d.y; }
-    else if (d.cls == 4) { nout = 0; }
-    else { kout[0] = a.N; kout[1] = a.N + 1; kout[2] = d.x; nout = 3; }
-    uint32_t ob[3][W4 + 1];
-#pragma unroll
-    for (int q = 0; q < 3; q++)
-#pragma unroll
-      for (int i = 0; i <= W4; i++) ob[q][i] = 0;
-    uint32_t bad = 0;
-    GroupWords<P, 0>::run([&](auto wc) {
-      constexpr int WI = decltype(wc)::value;
-      Word<NL> o[3];
-      finish_word<NL>(a, d, P, mode, ext, Pa[WI], acc[WI], NEWW[WI], o, grp * g + WI < W, bad);
-#pragma unroll
-      for (int q = 0; q < 3; q++)
-        if (q < nout) group_put<P, WI>(ob[q], o[q]);
-    });
-    if (mode == KMODE_SCRUB) {
-      if (bad) atomicAdd(a.counts + s, bad);
-      continue;
-    }
-#pragma unroll
-    for (int q = 0; q < 3; q++) {
-      if (q >= nout) break;
-      uint8_t* gq;  // address of byte byte0 of output q
-      uint64_t left;
-      if (mode == KMODE_PARTIAL) {  // slot of the owner of this word range
-        const int own = static_cast<int>(byte0 / a.range_bytes);
-        gq = (q == 0 ? a.part_p[own] : a.part_q[own]) + static_cast<uint64_t>(s) * a.part_stride +
-             (byte0 - static_cast<uint64_t>(own) * a.range_bytes);
-        left = a.pbytes > byte0 ? a.pbytes - byte0 : 0;
-      } else {
-        gq = const_cast<uint8_t*>(rptr(a, kout[q], s)) + byte0;
-        const uint64_t len = rlen(a, kout[q]);
-        left = len > byte0 ? len - byte0 : 0;
-      }
-      const int nb = static_cast<int>(left < static_cast<uint64_t>(GB) ? left : GB);
-      store_group<W4>(gq, nb, ob[q]);
-    }
-  }
-}
-
-template <int P>
-cudaError_t launch_p(const ZpArgs& a, int mode, cudaStream_t st, int num_sms) {
-  using GG = GP<P>;
-  uint64_t g0 = 0, g1 = ((8 * a.bytes + GG::n - 1) / GG::n + GG::g - 1) / GG::g;
-  if (mode == KMODE_COMBINE) {
-    g0 = a.range_lo / GG::GB;
-    g1 = std::min<uint64_t>(g1, (a.range_hi + GG::GB - 1) / GG::GB);
-    if (g1 < g0) g1 = g0;
-  }
-  const uint64_t total = (g1 - g0) * static_cast<uint64_t>(a.num_stripes);
-  const int threads = 128;
-  uint64_t blocks = (total + threads - 1) / threads;
-  const uint64_t cap = static_cast<uint64_t>(num_sms) * 16;
-  if (blocks > cap) blocks = cap;
-  if (blocks == 0) blocks = 1;
-  zp_generic_kernel<P><<<dim3(static_cast<unsigned>(blocks)), threads, 0, st>>>(a, mode);
-  return cudaGetLastError();
-}
-
-}  // namespace
+namespace gen {
+extern template cudaError_t launch_p<3>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<7>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<31>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<73>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<67>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<71>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<79>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<83>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<103>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<107>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<127>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<131>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<139>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<149>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<151>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<157>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<163>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<167>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<173>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<179>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<181>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<191>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<197>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<199>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<211>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<223>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<227>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<229>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<239>(const ZpArgs&, int, cudaStream_t, int);
+extern template cudaError_t launch_p<251>(const ZpArgs&, int, cudaStream_t, int);
+}  // namespace gen
 
 // The 26 primes whose period lcm(p-1, 32) exceeds 32 lanes, plus the fast primes without
 // extended-code kernels (3, 7, 31, 73: Theorem 25.3 fails, so never reached by a valid plan).
 cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, int num_sms) {
   switch (p) {
 #define ZP_GEN_CASE(PP) \
-  case PP: return launch_p<PP>(a, mode, st, num_sms);
+  case PP: return gen::launch_p<PP>(a, mode, st, num_sms);
     ZP_GEN_CASE(3) ZP_GEN_CASE(7) ZP_GEN_CASE(31) ZP_GEN_CASE(73)
     ZP_GEN_CASE(67) ZP_GEN_CASE(71) ZP_GEN_CASE(79) ZP_GEN_CASE(83) ZP_GEN_CASE(103) ZP_GEN_CASE(107)
     ZP_GEN_CASE(127) ZP_GEN_CASE(131) ZP_GEN_CASE(139) ZP_GEN_CASE(149) ZP_GEN_CASE(151) ZP_GEN_CASE(157)

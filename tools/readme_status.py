@@ -90,7 +90,7 @@ try:
     out.append(f"Other primes (`profiles/r01_primes.json`, c2 shape N = 12, 4 MiB × 256): the {len(fp)} primes added to the "
                f"fast path this round (every prime whose period lcm(p−1, 32) fits 32 lanes) encode at "
                f"{min(enc):.2f}–{max(enc):.2f} and recover at {min(rec):.2f}–{max(rec):.2f} of the copy rate; "
-               f"primes on the generic kernel (p = 67, 127 measured) run at {min(gen):.3f}–{max(gen):.3f}.")
+               f"the other {len(pr['generic_path'])} primes (generic kernel) run at {min(gen):.2f}–{max(gen):.2f}.")
 except FileNotFoundError:
     pass
 out.append("\n### NEXT-1 (update / scrub)\n")
