@@ -179,6 +179,10 @@ struct GP {
   static constexpr int g = 8 / ((n & 7) == 0 ? 8 : ((n & 3) == 0 ? 4 : 2));  // words per group
   static constexpr int GB = g * n / 8;                                      // bytes per group
   static constexpr int W4 = (GB + 3) / 4;                                   // 32-bit words per group
+  // CTAs of 128 threads per SM: 4 (<= 128 registers) while the g words x NL limbs of the two
+  // accumulators fit without spilling, else 3 (measured: p = 67, 127, 181 +25-50 % at 4 vs one
+  // unconstrained CTA; p = 251 spills 1.1 KB at 4 and runs best at 3)
+  static constexpr int MINB = NL * g <= 20 ? 4 : 3;
 };
 
 // Group range of one launch: all groups of the strip, or (combine) the groups of bytes
@@ -362,7 +366,7 @@ struct GroupWords {  // compile-time loop over the group's words
 };
 
 template <int P>
-__global__ void __launch_bounds__(128) zp_generic_kernel(const __grid_constant__ ZpArgs a, int mode) {
+__global__ void __launch_bounds__(128, GP<P>::MINB) zp_generic_kernel(const __grid_constant__ ZpArgs a, int mode) {
   using GG = GP<P>;
   constexpr int n = GG::n, NL = GG::NL, g = GG::g, GB = GG::GB, W4 = GG::W4;
   const uint64_t W = (8 * a.bytes + n - 1) / n;
