@@ -487,3 +487,56 @@ def test_rotation_unit_vectors(p):
         assert Pw == [1 << w for w in range(n)], a
         for w in range(n):
             assert Qw[w] == oracle.mul_xk(p, a, 1 << w), (p, a, w)
+
+
+# every prime instantiated in the p-templated generic kernel (zp_generic.cuh), each its own code
+GENERIC_ALL = [67, 71, 79, 83, 103, 107, 127, 131, 139, 149, 151, 157, 163, 167, 173, 179, 181, 191, 197,
+               199, 211, 223, 227, 229, 239, 251]
+
+
+@pytest.mark.parametrize("p", GENERIC_ALL)
+def test_generic_prime_encode_recover_scrub(p):
+    """Each generic-kernel prime (its own template instantiation: group geometry g = 2 or 4,
+    NL = 3..8 limbs): batched encode vs the oracle, every recovery class vs the originals on an
+    unaligned batch with a ragged tail, and a zero scrub count after encode."""
+    assert not R.has_fast_path(p)
+    N, nbytes, S = 9, 4 * 1024 + 77, 3
+    b = Batch(p, N, nbytes, S, offset=3, align=0)
+    b.fill_synthetic(seed=p, cfg=21)
+    b.par.fill_(0x6B)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    refs = []
+    for s in range(S):
+        data = synthetic.stripe_strips(p, 21, s, N, nbytes)
+        P, Q = oracle.encode(p, data, nbytes)
+        assert np.array_equal(b.numpy_strip(s, N), P) and np.array_equal(b.numpy_strip(s, N + 1), Q), (p, s)
+        refs.append(data + [P, Q])
+    cnt = torch.full((S,), 99, dtype=torch.int32, device="cuda")
+    plan.scrub_strided(*b.args(), cnt)
+    plan.sync()
+    assert cnt.cpu().tolist() == [0] * S
+    for pairs in ([(0, 8), (3, N), (5, N + 1)], [(N, N + 1), (1, 2), (7, N)]):
+        for s, (i, j) in enumerate(pairs):
+            _poison(b, s, (i, j))
+        plan.recover_strided(*b.args(), pairs)
+        plan.sync()
+        for s, (i, j) in enumerate(pairs):
+            for k in (i, j):
+                assert np.array_equal(b.numpy_strip(s, k), refs[s][k]), (p, s, i, j, k)
+    # small-write update of one strip per stripe (unaligned new rows) vs the oracle's re-encode
+    ns = nbytes + 5
+    newbuf = torch.zeros(S * ns + 16, dtype=torch.uint8, device="cuda")
+    new = newbuf[1:1 + S * ns].view(S, ns)
+    R.fill(new, ns, ns, nbytes, 1, S, p, 8, 0, 0, 0)
+    disks = [(4 * s + 2) % N for s in range(S)]
+    plan.update_strided(*b.args(), int(new.data_ptr()), ns, disks)
+    plan.sync()
+    for s in range(S):
+        data = refs[s][:N]
+        data[disks[s]] = new[s, :nbytes].cpu().numpy()
+        P, Q = oracle.encode(p, data, nbytes)
+        for k in range(N):
+            assert np.array_equal(b.numpy_strip(s, k), data[k]), (p, s, k)
+        assert np.array_equal(b.numpy_strip(s, N), P) and np.array_equal(b.numpy_strip(s, N + 1), Q), (p, s)
