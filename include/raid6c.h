@@ -85,7 +85,8 @@ size_t raid6c_parity_bytes(int p, size_t bytes);
 /* 1 if p is accepted (odd prime in [3,257]), else 0. */
 int raid6c_valid_p(int p);
 
-/* 1 if p has a specialised (compile-time-p) TMA kernel, 0 if it runs the generic kernel. */
+/* 1 if p runs the TMA fast-path kernel (the 28 primes whose period lcm(p-1, 32) fits 32 lanes),
+   0 if it runs the generic kernel (the other 26 odd primes <= 257). */
 int raid6c_has_fast_path(int p);
 
 /* 1 if p satisfies Theorem 25.3: gcd(X^p + 1, X^m + X + 1) = 1 for all
