@@ -521,8 +521,10 @@ struct SeriesPlan {
   static constexpr int CHAIN_COST = 10 * (top_bit(M) + c_popcount(M) - 1);
   // p = 61 (M = 31) keeps the chain: measured (r01 A/B), the two-level plan spills at the
   // 96-register cap of its 15-lane chunks and ran 1% slower on config 5; elsewhere it wins
-  // (c2 recover +1.5%, c4 DD +1.6%, p = 17 recover +3.2%).
-  static constexpr bool CHAIN = (M == 31) || CHAIN_COST < cost2(M2);
+  // (c2 recover +1.5%, c4 DD +1.6%, p = 17 recover +3.2%).  Long series (M > 50, p >= 101) take
+  // the chain: the model underrates the two-level plan's register cost there (measured recovery,
+  // chain vs two-level: p = 101 +5 %, 113 +8 %, 241 +10 %, 109 -1 %; 137, 193 already chain, +17-19 %).
+  static constexpr bool CHAIN = (M == 31) || M > 50 || CHAIN_COST < cost2(M2);
 };
 
 
