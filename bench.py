@@ -108,16 +108,21 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def pair_schedule(cfg, N, stripes, stripe0, step):
-    """Erasure pair of each stripe for a given step (host list of (i, j))."""
+def pair_of(cfg, N, stripes, g, step):
+    """Erasure pair (i < j) of global stripe g at `step` (stripes = the batch size per rank)."""
     import synthetic
-    allp = synthetic.all_pairs(N)
     if cfg == 4:  # double-data-disk recovery: (s mod 1653)-th data pair
         dd = [(i, j) for i in range(N) for j in range(i + 1, N)]
-        return [dd[(stripe0 + s) % len(dd)] for s in range(stripes)]
+        return dd[g % len(dd)]
     if cfg == 5:  # degraded stream: seeded class + indices per stripe
-        return [synthetic.erasure_pair(0, 5, stripe0 + s + step * stripes, N) for s in range(stripes)]
-    return [allp[(stripe0 + s + 37 * step) % len(allp)] for s in range(stripes)]
+        return synthetic.erasure_pair(0, 5, g + step * stripes, N)
+    allp = synthetic.all_pairs(N)
+    return allp[(g + 37 * step) % len(allp)]
+
+
+def pair_schedule(cfg, N, stripes, stripe0, step):
+    """Erasure pair of each stripe for a given step (host list of (i, j))."""
+    return [pair_of(cfg, N, stripes, stripe0 + s, step) for s in range(stripes)]
 
 
 def alg_bytes_recover(N, nbytes, pb, pairs):
@@ -136,14 +141,48 @@ def traffic_from_profile(cfg):
         return None
 
 
-# ====================================================================== our arm
-def run_ours(args):
+# ====================================================================== multi-rank plumbing
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def self_launch(args):
+    """--gpus N (N > 1) without a torchrun environment: bring the N ranks up ourselves (one process
+    per GPU through torch.distributed.run on 127.0.0.1) and return their exit status.  Never falls
+    back to one rank: with NCCL, fewer visible GPUs than N is an error (exit 2); a rank that fails
+    fails the launch.  NCCL's communicator log (NCCL_DEBUG=INFO, INIT subsystem) goes to stderr so
+    the rank count can be read off it; the JSON line (rank 0) stays the only thing on stdout."""
+    import torch
+    n = args.gpus
+    if args.dist_backend == "nccl" and torch.cuda.device_count() < n:
+        print(f"error: --gpus {n} needs {n} visible GPUs for NCCL, found {torch.cuda.device_count()} "
+              f"(use --dist-backend gloo to rehearse {n} ranks on fewer GPUs)", file=sys.stderr)
+        return 2
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"note: launching {n} ranks: {' '.join(cmd[2:6])}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=env).returncode
+
+
+def init_ranks(args):
+    """Rank setup shared by every mode: device, process group (NCCL, or gloo for rehearsals), and
+    a check that exactly --gpus ranks came up.  Returns (rank, world, local, dev, rank_info)."""
     import torch
     import torch.distributed as dist
-    from paper_cs_0611109_b200 import raid6c as R
-    from paper_cs_0611109_b200 import shard
-
     rank, world, local = _env_rank()
+    if world != args.gpus:
+        print(f"error: {world} rank(s) running but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     local = local % torch.cuda.device_count()  # (only differs in the 1-GPU multi-rank rehearsal)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -152,6 +191,98 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
         else:  # gloo: rehearse the multi-rank path with several ranks on one GPU (host-side collectives only)
             dist.init_process_group("gloo")
+    props = torch.cuda.get_device_properties(dev)
+    me = {"rank": rank, "cuda_device": local, "uuid": str(getattr(props, "uuid", ""))[:13], "pid": os.getpid()}
+    info = [me]
+    if world > 1:
+        info = [None] * world
+        dist.all_gather_object(info, me)
+    return rank, world, local, dev, {"ranks_up": len(info), "distinct_gpus": len({i["uuid"] for i in info}),
+                                     "backend": args.dist_backend if world > 1 else None, "ranks": info}
+
+
+def gather_dict(d):
+    """Union of per-rank dicts on every rank (all_gather_object; identity at world size 1)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return dict(d)
+    parts = [None] * dist.get_world_size()
+    dist.all_gather_object(parts, d)
+    out = {}
+    for part in parts:
+        out.update(part)
+    return out
+
+
+# ====================================================================== digests (harness)
+def gpu_strip_digests(R, torch, data, par, S, N, ss, ps, nbytes, pb, stream, dev):
+    """Per-strip digests of S stripes: host list of S lists [d_0 .. d_{N-1}, P, Q] (python ints).
+    raid6c_digest kernels on `stream`; see synthetic/digest.py for the definition."""
+    dd = torch.empty(S * N, dtype=torch.int64, device=dev)
+    dp = torch.empty(S * 2, dtype=torch.int64, device=dev)
+    R.digest(data, ss, N * ss, nbytes, N, S, dd, stream)
+    R.digest(par, ps, 2 * ps, pb, 2, S, dp, stream)
+    stream.synchronize()
+    a, b = dd.view(S, N).cpu().tolist(), dp.view(S, 2).cpu().tolist()
+    m = (1 << 64) - 1
+    return [[v & m for v in a[s]] + [v & m for v in b[s]] for s in range(S)]
+
+
+def digest_all(gdig):
+    """One digest of every strip of the run, in global stripe order (comparable across G)."""
+    import synthetic
+    return "%016x" % synthetic.combine_digests([v for g in sorted(gdig) for v in gdig[g]])
+
+
+def oracle_digest_check(p, N, nbytes, cfg, sparse_mode, gdig, pairs_by_g, k, threads):
+    """The cpu_baseline leg: the oracle, as it stands, on k sampled stripes at FULL size (spread
+    over the run's global stripes, so every rank's shard is sampled): encode, plus the recovery of
+    the stripe's erasure pair.  Its outputs, reduced to digests, are compared with the GPU's
+    (gdig[g] = [d_0..d_{N-1}, P, Q] digests after the run).  Returns (verified part, cpu_baseline)."""
+    import synthetic
+    from tests import oracle_sample as OS
+    gs = sorted(gdig)
+    picks = [gs[i] for i in OS.sample_stripes(len(gs), k)] if k > 0 else []
+    items = [(g, [tuple(pairs_by_g[g])] if pairs_by_g.get(g) is not None else []) for g in picks]
+    sparse_of = (lambda g: sparse_mode == 1 or (sparse_mode == 2 and g % 2 == 1))
+    dig, info = OS.stripe_digests(p, N, nbytes, cfg, items, sparse_of=sparse_of, threads=threads)
+    ok, by_class, bad = 0, {}, []
+    for g, prs in items:
+        d, o = gdig[g], dig[g]
+        good = d[N] == o["P"] and d[N + 1] == o["Q"]
+        for (x, y) in prs:
+            good = good and d[x] == o[(x, y, x)] and d[y] == o[(x, y, y)]
+        cls = synthetic.pair_class(N, *prs[0]) if prs else "encode"
+        c = by_class.setdefault(cls, [0, 0])
+        c[1] += 1
+        if good:
+            ok += 1
+            c[0] += 1
+        else:
+            bad.append(g)
+    ver = {"oracle_digest_stripes": ok, "oracle_digest_sampled": len(items),
+           "oracle_digest_by_class": {kk: {"ok": v[0], "sampled": v[1]} for kk, v in sorted(by_class.items())},
+           "oracle_digest_failed_stripes": bad[:16]}
+    per_thread_s = info["oracle_s"] / max(1, info["threads"])
+    base = {"value": round(info["user_bytes"] / max(per_thread_s, 1e-9) / 1e9, 6), "unit": "GB/s",
+            "cores": info["threads"], "kind": "oracle",
+            "sample": (f"{len(items)} stripes at full size ({N} x {nbytes} B), oracle encode"
+                       f"{' + the stripe' + chr(39) + 's recovery' if any(pr for _, pr in items) else ''}, run on "
+                       f"{info['segment_bytes']}-byte word-aligned segments over {info['threads']} host threads; "
+                       f"value = user bytes / (oracle-call seconds / threads); the same outputs verify the GPU "
+                       f"(verified.oracle_digest_*)"),
+            "seconds": round(info["wall_s"], 2), "oracle_call_s": round(info["oracle_s"], 2)}
+    return ver, base
+
+
+# ====================================================================== our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_cs_0611109_b200 import raid6c as R
+    from paper_cs_0611109_b200 import shard
+
+    rank, world, local, dev, rank_info = init_ranks(args)
     c = CONFIGS[args.config]
     p, N, S = args.prime or c["p"], args.data_strips or c["N"], args.stripes or c["stripes"]
     nbytes = args.strip_bytes or c["nbytes"]
@@ -247,24 +378,62 @@ def run_ours(args):
     per_rank_ms = [round(x, 3) for x in per_rank]
     elapsed_ms = max(per_rank)
 
-    # ---------------------------------------------------------------- verification
-    verified = None
+    # ---------------------------------------------------------------- verification (untimed)
+    verified, base_line = None, None
     if args.verify:
-        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-        torch.cuda.synchronize(dev)  # cnt is zeroed on torch's stream; the compare runs on `stream`
+        cnt = torch.zeros(3, dtype=torch.int64, device=dev)
+        torch.cuda.synchronize(dev)  # cnt is zeroed on torch's stream; the compares run on `stream`
         if do_rec:
-            # ref snapshot was taken after warm-up steps; data/parity must be bit-identical
-            R.count_mismatch(data, ref_data, data.numel(), cnt, stream)
-            R.count_mismatch(par, ref_par, par.numel(), cnt, stream)
+            # (1) round trip: the snapshot was taken after the warm-up steps; every timed step
+            # rewrote its lost strips in place, so data and parity must be bit-identical
+            R.count_mismatch(data, ref_data, data.numel(), cnt[0:1], stream)
+            R.count_mismatch(par, ref_par, par.numel(), cnt[0:1], stream)
+            # (2) the last step's recovery once more with its lost strips POISONED first (their old
+            # contents are never read: PAPER.md:380-401 makes them the unknowns), compared with the
+            # snapshot -- a recovery that wrote nothing or the wrong bytes fails here
+            last = pair_lists[-1]
+            dl = [s_ * N + k for s_, pr in enumerate(last) for k in pr if k < N]
+            pl = [s_ * 2 + (k - N) for s_, pr in enumerate(last) for k in pr if k >= N]
+            with torch.cuda.stream(stream):
+                if dl:
+                    data.view(S * N, ss).index_fill_(0, torch.tensor(dl, device=dev), 0xA5)
+                if pl:
+                    par.view(S * 2, ps).index_fill_(0, torch.tensor(pl, device=dev), 0xA5)
+                plan.recover_strided(*enc_args, pair_dev[-1])
+                R.count_mismatch(data, ref_data, data.numel(), cnt[1:2], stream)
+                R.count_mismatch(par, ref_par, par.numel(), cnt[1:2], stream)
+        poisoned = (len(dl) * nbytes + len(pl) * pb) if do_rec else 0
+        if do_enc:
+            # (3) a fresh encode over poisoned parity must rewrite P and Q exactly
+            with torch.cuda.stream(stream):
+                par.fill_(0xA5)
+                plan.encode_strided(*enc_args)
+                if do_rec:
+                    R.count_mismatch(par, ref_par, par.numel(), cnt[2:3], stream)
         stream.synchronize()
-        mism = int(cnt.item())
-        checked = 2 * data.numel() if do_rec else 0
-        oracle_ok = None
-        if rank == 0 and args.oracle_check:
-            oracle_ok = (rs_sample_check if rs else oracle_sample_check)(p, N, nbytes, args.config, c["sparse"],
-                                                                        stripe0, par)
-        tot = shard.sum_over_ranks([mism, checked], dev)
-        verified = {"mismatched_bytes": tot[0], "checked_bytes": tot[1], "oracle_segments_match": oracle_ok}
+        mism = [int(v) for v in cnt.tolist()]
+        tot = shard.sum_over_ranks(mism + [2 * data.numel() if do_rec else 0, poisoned], dev)
+        verified = {"mismatched_bytes": tot[0], "checked_bytes": tot[3],
+                    "poisoned_recovery": {"poisoned_bytes": tot[4], "mismatched_bytes": tot[1]} if do_rec else None,
+                    "fresh_encode_mismatched_bytes": tot[2] if (do_enc and do_rec) else None}
+        # (4) per-strip digests of every stripe (GPU), gathered; the oracle sample below checks them
+        if not rs:
+            dg = gpu_strip_digests(R, torch, data, par, S, N, ss, ps, nbytes, pb, stream, dev)
+            gdig = gather_dict({stripe0 + s_: dg[s_] for s_ in range(S)})
+            pairs_by_g = gather_dict({stripe0 + s_: (pair_lists[-1][s_] if do_rec else None) for s_ in range(S)})
+            verified["digest_all"] = digest_all(gdig)
+            if rank == 0 and args.cpu_baseline:
+                ver, base_line = oracle_digest_check(p, N, nbytes, args.config, c["sparse"], gdig, pairs_by_g,
+                                                     32 if args.oracle_stripes is None else args.oracle_stripes,
+                                                     args.cpu_threads)
+                verified.update(ver)
+        elif rank == 0 and args.oracle_check:
+            verified["oracle_segments_match"] = rs_sample_check(p, N, nbytes, args.config, c["sparse"], stripe0, par)
+        verified["ok"] = (verified["mismatched_bytes"] == 0
+                          and (verified["poisoned_recovery"] or {}).get("mismatched_bytes", 0) == 0
+                          and not verified.get("fresh_encode_mismatched_bytes")
+                          and verified.get("oracle_digest_stripes", 0) == verified.get("oracle_digest_sampled", 0)
+                          and verified.get("oracle_segments_match", True) is not False)
         del ref_data, ref_par
 
     # ---------------------------------------------------------------- e2e (host buffers, public API)
@@ -316,18 +485,22 @@ def run_ours(args):
                    "stripes_per_gpu": S, "ops": ops, "parallelism": f"stripe-sharded x{world} (no data-path collective)",
                    "l2": "working set >= 1 GiB >> 126 MB L2 (no flush needed)"},
         "roofline": roof, "kernels": per_kernel, "gpu_launches": launches, "clocks": clk,
-        "per_rank_ms": per_rank_ms,
+        "per_rank_ms": per_rank_ms, "ranks": rank_info,
         "verified": verified, "e2e": e2e,
         "fast_path": R.has_fast_path(p), "code": args.code,
     }
-    if rank == 0 and world == 1 and args.cpu_baseline and not rs:  # the oracle baseline: rank 0 at N=1 only
-        line["cpu_baseline"] = cpu_baseline(args, p, N, nbytes, args.config, c["sparse"])
+    if args.dump_steps:  # per-step launch times (diagnosis of run-to-run spread)
+        line["step_ms"] = {k: [round(x, 4) for x in v] for k, v in launch_ms.items() if v}
+    if base_line is not None:  # the oracle baseline (rank 0, every N): the digest sample above
+        line["cpu_baseline"] = base_line
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if verified is not None and not verified["ok"]:
+        sys.exit(3)  # a line whose results do not verify is not a measurement
 
 
 FULL_STRIPES = {2: 256, 4: 4096, 5: 1000}  # BASELINE.json configs[1], [3], [4]: whole-config stripe counts
@@ -441,24 +614,21 @@ def run_full(args):
     the recovery's input), poison the wave's lost strips (untimed), recover them in place (timed),
     scrub the wave (untimed).  The scrub proves every recovery: with the N surviving strips given,
     the lost pair is the unique solution of both parity equations (Lemma 23.2),
-    so a stripe with zero violating words after recovery was rebuilt exactly.  Sampled P/Q
-    segments are compared with the CPU oracle.  value = user bytes of all ranks / max-rank sum of
-    the timed kernel intervals (CUDA events on the plan's stream)."""
+    so a stripe with zero violating words after recovery was rebuilt exactly.  After each wave
+    the per-strip digests of all its stripes are taken (untimed) and gathered over the ranks;
+    for --oracle-stripes sampled stripes (spread over every rank's shard) the oracle's full-size
+    outputs (encode + the stripe's recovery) are reduced to digests on the host cores and must
+    match (the cpu_baseline leg).  `verified.digest_all` digests every strip of the run in global
+    stripe order, so runs at G = 1, 2, 4, 8 can be compared.  value = user bytes of all ranks /
+    max-rank sum of the timed kernel intervals (CUDA events on the plan's stream)."""
     import torch
-    import torch.distributed as dist
     import synthetic
     from paper_cs_0611109_b200 import raid6c as R
     from paper_cs_0611109_b200 import shard
 
-    rank, world, local = _env_rank()
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group("gloo")
+    if args.config == 2:
+        return run_c2_literal(args)
+    rank, world, local, dev, rank_info = init_ranks(args)
     if args.config not in FULL_STRIPES:
         raise SystemExit(f"--full applies to configs {sorted(FULL_STRIPES)}")
     c = CONFIGS[args.config]
@@ -488,6 +658,7 @@ def run_full(args):
                 torch.tensor(dl, dtype=torch.int64, device=dev), torch.tensor(pl, dtype=torch.int64, device=dev))
 
     tables = [wave_tables(w0, min(wave, hi - w0)) for w0 in range(lo, hi, wave)]
+    wave_digests = {}
     torch.cuda.synchronize(dev)
 
     def run_wave(tab):
@@ -509,12 +680,17 @@ def run_full(args):
             e[3].record(stream)
             plan.scrub_strided(*args_, counts)
             bad_total.add_(counts[:n].sum())
+        if args.verify:  # digests of the wave after its recovery (untimed; waits for the wave)
+            dg = gpu_strip_digests(R, torch, data, par, n, N, ss, ps, nbytes, pb, stream, dev)
+            for s_ in range(n):
+                wave_digests[w0 + s_] = dg[s_]
         return e
 
     for _ in range(args.warmup):  # warm-up on the first wave (not counted)
         run_wave(tables[0])
     stream.synchronize()
     bad_total.zero_()
+    wave_digests.clear()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -537,11 +713,16 @@ def run_full(args):
     enc_ms = sum(e[0].elapsed_time(e[1]) for e in evs) if do_enc else 0.0
     rec_ms = sum(e[2].elapsed_time(e[3]) for e in evs)
     timed_ms = enc_ms + rec_ms
-    oracle_ok = None
-    if rank == 0 and args.oracle_check:
-        last_w0 = lo + ((hi - lo - 1) // wave) * wave
-        oracle_ok = oracle_sample_check(p, N, nbytes, args.config, c["sparse"], last_w0,
-                                        par[:min(wave, hi - last_w0)])
+    ver, base_line = {}, None
+    if args.verify:
+        gdig = gather_dict(wave_digests)
+        pairs_by_g = gather_dict({g: pr for tab in tables for g, pr in zip(range(tab[0], tab[0] + tab[1]), tab[2])})
+        ver["digest_all"] = digest_all(gdig)
+        ver["digested_stripes"] = len(gdig)
+        if rank == 0 and args.cpu_baseline:
+            v, base_line = oracle_digest_check(p, N, nbytes, args.config, c["sparse"], gdig, pairs_by_g,
+                                               64 if args.oracle_stripes is None else args.oracle_stripes, args.cpu_threads)
+            ver.update(v)
     bad = int(bad_total.item())
     t_max = shard.max_over_ranks(timed_ms, dev)
     enc_max = shard.max_over_ranks(enc_ms, dev)
@@ -578,16 +759,198 @@ def run_full(args):
                      "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                      "peak_source": peak_src},
         "kernels": kern, "gpu_launches": launches, "clocks": clk, "wall_s_rank0": round(wall, 2),
-        "classes": dict(zip(("DD", "DP", "DQ", "PQ"), tot[2:])),
-        "verified": {"stripes": nst_all, "scrub_bad_words_after_recovery": bad_all,
-                     "oracle_segments_match": oracle_ok},
+        "classes": dict(zip(("DD", "DP", "DQ", "PQ"), tot[2:])), "ranks": rank_info,
+        "verified": dict({"stripes": nst_all, "scrub_bad_words_after_recovery": bad_all}, **ver),
     }
+    line["verified"]["ok"] = bad_all == 0 and ver.get("oracle_digest_stripes", 0) == ver.get("oracle_digest_sampled", 0)
+    if base_line is not None:
+        line["cpu_baseline"] = base_line
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:
+        import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+    if not line["verified"]["ok"]:
+        sys.exit(3)
+
+
+def run_c2_literal(args):
+    """--config 2 --full: BASELINE.json configs[1] as written -- 256 stripes of p=13, N=12, 4 MiB
+    (block-sharded over the ranks), encode, then recovery of ALL 91 erasure pairs in every stripe:
+    91 launches, one pair per launch (classes per the paper's reconstruction table, PAPER.md:
+    1186-1198: 66 DD, 12 DP, 12 DQ, 1 PQ).  Per pair (untimed around the timed launch): the two
+    lost strips of every stripe are poisoned (0xA5), the recovery runs (CUDA events), a scrub counts
+    words violating either parity equation (zero = exact, Lemma 23.2), and the two rebuilt strips of
+    every stripe are digested on the GPU.  The rebuilt digests must equal the stripe's digests
+    before the run (data: the input; P, Q: the encode's), and the encode's P, Q digests of ALL 256
+    stripes must equal the oracle's (a full oracle encode of config 2 on the host cores); the oracle
+    also rebuilds each of the 91 pairs on one stripe, whose digests must match the GPU's.  Reports
+    the per-class recovery GB/s."""
+    import torch
+    import synthetic
+    from paper_cs_0611109_b200 import raid6c as R
+    from paper_cs_0611109_b200 import shard
+
+    rank, world, local, dev, rank_info = init_ranks(args)
+    c = CONFIGS[2]
+    p, N, nbytes = c["p"], c["N"], c["nbytes"]
+    total = args.stripes or FULL_STRIPES[2]
+    lo, hi = shard.block_range(rank, world, total)
+    S = hi - lo
+    pb = R.parity_bytes(p, nbytes)
+    ss, ps = R.aligned_stride(nbytes), R.aligned_stride(pb)
+    stream = torch.cuda.Stream(device=dev)
+    data = torch.empty((max(S, 1), N, ss), dtype=torch.uint8, device=dev)
+    par = torch.zeros((max(S, 1), 2, ps), dtype=torch.uint8, device=dev)
+    counts = torch.zeros(max(S, 1), dtype=torch.int32, device=dev)
+    plan = R.Plan(p, N, nbytes, local, stream)
+    a = (int(data.data_ptr()), ss, N * ss, int(par.data_ptr()), int(par.data_ptr()) + ps, 2 * ps, S)
+    R.fill(data, ss, N * ss, nbytes, N, S, 0, 2, lo, 0, 0, stream)
+    flat_d, flat_p = data.view(-1, ss), par.view(-1, ps)
+    allp = synthetic.all_pairs(N)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            plan.encode_strided(*a)
+            plan.recover_strided(*a, [allp[0]])
+    din = gpu_strip_digests(R, torch, data, par, S, N, ss, ps, nbytes, pb, stream, dev)  # P, Q = encode's
+    torch.cuda.synchronize(dev)
+    shard.max_over_ranks(0.0, dev)  # barrier
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    launches0 = R.launch_count()
+    enc_ms, rec_ms, bad, rebuilt = [], {}, 0, {}
+    with torch.cuda.stream(stream):
+        for _ in range(max(1, args.steps)):  # the encode, timed --steps times (mean reported)
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            plan.encode_strided(*a)
+            e1.record(stream)
+            enc_ms.append((e0, e1))
+        for (x, y) in allp:
+            for k in (x, y):  # poison the lost strips of every stripe (never read by the recovery)
+                if k < N:
+                    flat_d[k::N][:S].fill_(0xA5)
+                else:
+                    flat_p[k - N::2][:S].fill_(0xA5)
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            plan.recover_strided(*a, [(x, y)])
+            e1.record(stream)
+            rec_ms[(x, y)] = (e0, e1)
+            plan.scrub_strided(*a, counts)
+            bad += int(counts[:S].sum().item())  # (syncs: the loop is untimed around the events)
+            for k in (x, y):
+                dk = torch.empty(S, dtype=torch.int64, device=dev)
+                if k < N:
+                    R.digest(int(data.data_ptr()) + k * ss, N * ss, N * ss, nbytes, 1, S, dk, stream)
+                else:
+                    R.digest(int(par.data_ptr()) + (k - N) * ps, 2 * ps, 2 * ps, pb, 1, S, dk, stream)
+                rebuilt[(x, y, k)] = dk
+    stream.synchronize()
+    launches = R.launch_count() - launches0
+    clk = clocks.stop()
+    m = (1 << 64) - 1
+    enc_t = [e0.elapsed_time(e1) for e0, e1 in enc_ms]
+    rec_t = {pr: e0.elapsed_time(e1) for pr, (e0, e1) in rec_ms.items()}
+    # every rebuilt strip of every stripe equals the stripe before the run (digest)
+    rb_bad = 0
+    for (x, y, k), dk in rebuilt.items():
+        vals = [v & m for v in dk.tolist()]
+        rb_bad += sum(1 for s_ in range(S) if vals[s_] != din[s_][k])
+    # per-class sums (max over ranks), user bytes of all ranks
+    cls_ms = {}
+    for pr, t in rec_t.items():
+        cls_ms.setdefault(synthetic.pair_class(N, *pr), []).append(t)
+    names = ("DD", "DP", "DQ", "PQ")
+    sums = [shard.max_over_ranks(sum(cls_ms.get(k, [])), dev) for k in names]
+    enc_mean = shard.max_over_ranks(statistics.mean(enc_t), dev)
+    rec_total = shard.max_over_ranks(sum(rec_t.values()), dev)
+    tot = shard.sum_over_ranks([bad, rb_bad, S], dev)
+    gdig = gather_dict({lo + s_: din[s_] for s_ in range(S)})
+    ver = {"stripes": tot[2], "pairs": len(allp), "scrub_bad_words_after_recovery": tot[0],
+           "rebuilt_strip_digest_mismatches": tot[1], "rebuilt_strips_checked": 2 * len(allp) * tot[2],
+           "digest_all": digest_all(gdig)}
+    base_line = None
+    if rank == 0 and args.cpu_baseline:
+        # the oracle: a full encode of every stripe (P, Q digests) ...
+        dig, info = _c2_oracle(p, N, nbytes, sorted(gdig), allp, args.cpu_threads)
+        enc_bad = [g for g in gdig if gdig[g][N] != dig[g]["P"] or gdig[g][N + 1] != dig[g]["Q"]]
+        # ... and each of the 91 pairs rebuilt by the oracle on one stripe, vs the GPU's rebuilt strips
+        pr_bad = []
+        for i, (x, y) in enumerate(allp):
+            g = sorted(gdig)[(7 * i) % len(gdig)]
+            for k in (x, y):
+                if dig[g][(x, y, k)] != gdig[g][k]:
+                    pr_bad.append((g, x, y, k))
+        ver.update({"oracle_encode_digest_stripes": len(gdig) - len(enc_bad), "oracle_encode_sampled": len(gdig),
+                    "oracle_pair_digests_ok": 2 * len(allp) - len(pr_bad), "oracle_pair_digests": 2 * len(allp),
+                    "oracle_failed": (enc_bad + pr_bad)[:16]})
+        per_thread_s = info["oracle_s"] / max(1, info["threads"])
+        base_line = {"value": round(info["user_bytes"] / per_thread_s / 1e9, 6), "unit": "GB/s",
+                     "cores": info["threads"], "kind": "oracle",
+                     "sample": (f"full oracle encode of all {len(gdig)} stripes + each of the {len(allp)} pairs "
+                                f"rebuilt on one stripe (full 4 MiB strips, {info['segment_bytes']}-byte word-aligned "
+                                f"segments over {info['threads']} threads); value = user bytes / (oracle-call "
+                                f"seconds / threads)"),
+                     "seconds": round(info["wall_s"], 2), "oracle_call_s": round(info["oracle_s"], 2)}
+    ok = tot[0] == 0 and tot[1] == 0 and (base_line is None or (not ver["oracle_failed"]))
+    ver["ok"] = ok
+    alg = tot[2] * (N * nbytes + 2 * pb)
+    user = tot[2] * N * nbytes
+    peak, peak_src = measured_peak()
+    per_class = {}
+    for k, t in zip(names, sums):
+        npairs = len(cls_ms.get(k, []))
+        if npairs:
+            per_class[k] = {"pairs": npairs, "sum_ms": round(t, 3), "ms_per_launch": round(t / npairs, 4),
+                            "user_GBps": round(user * npairs / (t / 1e3) / 1e9, 1),
+                            "achieved_GBps": round(alg * npairs / (t / 1e3) / 1e9, 1),
+                            "frac_of_peak": round(alg * npairs / (t / 1e3) / 1e9 / peak, 4)}
+    t_all = enc_mean + rec_total
+    value = user * (1 + len(allp)) / (t_all / 1e3) / 1e9
+    dom = max(per_class, key=lambda k: per_class[k]["ms_per_launch"])
+    line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": 1 + len(allp),
+            "warmup": args.warmup, "ms_per_step": round(t_all, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32 (bitwise GF(2) words)",
+            "data": "synthetic (seeded SplitMix64 counter generator, generated on device)",
+            "config": {"workload": f"c2 literal: {total} stripes of p=13 N=12 4 MiB, encode + all 91 pairs recovered "
+                                   f"in every stripe (one pair per launch), block-sharded over {world} GPU(s)",
+                       "p": p, "N": N, "strip_bytes": nbytes, "parity_bytes": pb, "stripes_total": total,
+                       "parallelism": f"stripe-sharded x{world} (no data-path collective)",
+                       "l2": "14 GiB per launch >> 126 MB L2 (no flush needed)",
+                       "timed": "1 encode (mean of --steps) + 91 recovery launches; poisoning, scrub, digests untimed"},
+            "roofline": {"kernel": f"zp_kernel<13,1> ({dom} recovery)", "bound": "hbm",
+                         "achieved": per_class[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
+                         "frac": per_class[dom]["frac_of_peak"], "peak_source": peak_src},
+            "kernels": {"encode": {"ms": round(enc_mean, 4),
+                                   "achieved_GBps": round(alg / (enc_mean / 1e3) / 1e9, 1),
+                                   "frac_of_peak": round(alg / (enc_mean / 1e3) / 1e9 / peak, 4)},
+                        "recover_by_class": per_class},
+            "gpu_launches": launches, "clocks": clk, "ranks": rank_info, "verified": ver}
+    if base_line is not None:
+        line["cpu_baseline"] = base_line
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    if not ok:
+        sys.exit(3)
+
+
+def _c2_oracle(p, N, nbytes, stripes, allp, threads):
+    """Oracle digests for run_c2_literal: every stripe encoded; pair i rebuilt on stripe (7i mod S)."""
+    from tests import oracle_sample as OS
+    want = {g: [] for g in stripes}
+    for i, pr in enumerate(allp):
+        want[stripes[(7 * i) % len(stripes)]].append(pr)
+    return OS.stripe_digests(p, N, nbytes, 2, list(want.items()), threads=threads)
 
 
 def run_xgpu(args):
@@ -936,30 +1299,6 @@ def rs_sample_check(p, N, nbytes, cfg, sparse_mode, stripe0, par):
     return ok
 
 
-def oracle_sample_check(p, N, nbytes, cfg, sparse_mode, stripe0, par):
-    """Sampled word-aligned P/Q segments of two stripes against the CPU oracle."""
-    import numpy as np
-    import oracle
-    import synthetic
-    n = p - 1
-    ok = True
-    for s in (0, par.shape[0] - 1):
-        gs = stripe0 + s
-        sparse = sparse_mode == 1 or (sparse_mode == 2 and gs % 2 == 1)
-        W = (8 * nbytes + n - 1) // n
-        for g0 in (0, (W // 8) // 2, max(0, W // 8 - 2)):
-            b0 = g0 * n
-            b1 = min(nbytes, b0 + 2 * n)
-            if g0 == max(0, W // 8 - 2):
-                b1 = nbytes
-            segs = [synthetic.strip_bytes(0, cfg, gs, k, nbytes, sparse, lo=b0, hi=b1) for k in range(N)]
-            P, Q = (oracle.encode_ext if N > p else oracle.encode)(p, segs, b1 - b0)
-            e = b0 + P.size
-            ok &= bool(np.array_equal(par[s, 0, b0:e].cpu().numpy(), P))
-            ok &= bool(np.array_equal(par[s, 1, b0:e].cpu().numpy(), Q))
-    return ok
-
-
 # ====================================================================== oracle (CPU) arm
 def _oracle_work(p, N, nbytes, cfg, sparse_mode, budget_s, max_threads):
     """Time the oracle as it stands on a bounded sample of the same workload: per stripe,
@@ -1009,12 +1348,6 @@ def _oracle_work(p, N, nbytes, cfg, sparse_mode, budget_s, max_threads):
               f"({'encode' if ops != 'rec' else ''}{' + ' if ops == 'enc+rec' or ops == 'enc+dd' else ''}"
               f"{'one recovery' if ops != 'enc' else ''} each), bit-array oracle, {threads} threads")
     return users, wall, threads, sample
-
-
-def cpu_baseline(args, p, N, nbytes, cfg, sparse_mode):
-    users, wall, threads, sample = _oracle_work(p, N, nbytes, cfg, sparse_mode, args.cpu_budget, args.cpu_threads)
-    return {"value": round(users / wall / 1e9, 6), "unit": "GB/s", "cores": threads, "kind": "oracle",
-            "sample": sample, "seconds": round(wall, 2)}
 
 
 def run_reference(args):
@@ -1076,13 +1409,15 @@ def main():
     ap.add_argument("--cpu-threads", type=int, default=64)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: rehearse N>1 on fewer GPUs (ranks share devices; timing not meaningful)")
+    ap.add_argument("--dump-steps", action="store_true", help="add every timed step's launch times to the line")
+    ap.add_argument("--oracle-stripes", type=int, default=None,
+                    help="stripes of the oracle digest sample (cpu_baseline leg): default 32, --full c4/c5 64")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warm-up raised to 3 (timing rule)", file=sys.stderr)
         args.warmup = 3
-    if args.gpus > 1 and _env_rank()[1] == 1:
-        print(f"note: --gpus {args.gpus} without a torchrun launch runs one rank (launch with "
-              f"python -m torch.distributed.run --nproc-per-node {args.gpus} ...)", file=sys.stderr)
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))  # N ranks, one process per GPU (never silently one rank)
     if args.impl == "reference":
         run_reference(args)
     elif args.op != "step":

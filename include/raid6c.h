@@ -250,7 +250,8 @@ raid6c_status raid6c_partial_strided(raid6c_plan plan, const uint8_t *const *str
                                      size_t part_stride, size_t range_bytes);
 
 /* Combine + solve for bytes [range_lo, range_hi) of every stripe (range_lo a multiple of the
- * range size; range_hi <= parity_bytes).  src_p / src_q: HOST arrays of num_sources DEVICE
+ * range granule; range_hi a multiple of it too, or equal to parity_bytes -- anything else is
+ * RAID6C_E_SIZE, since the kernels work in whole granules).  src_p / src_q: HOST arrays of num_sources DEVICE
  * pointers; source r holds stripe s's partial of this range at src_p[r] + s*part_stride.
  * strips: HOST array of N+2 DEVICE pointers (global index, strides as in the partial call);
  * only the two output strips of each stripe are written (lost strips; P and Q for an
@@ -307,6 +308,18 @@ raid6c_status raid6c_fill(uint8_t *dst, size_t strip_stride, size_t stripe_strid
  * (a DEVICE uint64).  Stream-ordered. */
 raid6c_status raid6c_count_mismatch(const uint8_t *a, const uint8_t *b, size_t len,
                                     uint64_t *count_dev, void *stream);
+
+/* Per-strip 64-bit digests of DEVICE strips (test / bench harness, not the method; host
+ * version: synthetic/digest.py).  For s in [0, nstripes), t in [0, nstrips), the `len` bytes at
+ * src + s*stripe_stride + t*strip_stride get
+ *   digests_dev[s*nstrips + t] = mix64(len ^ 0xBB67AE8584CAA73B)
+ *                                + sum_k mix64(w_k + k*0x9E3779B97F4A7C15 + 0x6A09E667F3BCC909)  (mod 2^64),
+ * w_k the little-endian u64 of bytes [8k, 8k+8) (zero past len), mix64 = SplitMix64's finalizer.
+ * A changed word always changes the digest (mix64 is a bijection), so equal digests of a GPU
+ * strip and an oracle strip computed elsewhere stand for equal bytes (up to 2^-64 per pair).
+ * digests_dev is a DEVICE array of nstrips*nstripes uint64, overwritten.  Stream-ordered. */
+raid6c_status raid6c_digest(const uint8_t *src, size_t strip_stride, size_t stripe_stride, size_t len,
+                            int nstrips, int nstripes, uint64_t *digests_dev, void *stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

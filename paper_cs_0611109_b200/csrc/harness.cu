@@ -1,6 +1,8 @@
 // harness.cu -- bench/test harness kernels (NOT the method): the synthetic generator of
 // synthetic/gen.py re-implemented on the device (checked bit-for-bit against the numpy
-// version by tests/test_gpu_parity.py::test_fill_matches_numpy_generator) and a byte compare.
+// version by tests/test_gpu_parity.py::test_fill_matches_numpy_generator), a byte compare, and
+// a per-strip 64-bit digest (synthetic/digest.py; tests/test_gpu_digest.py) that lets full-size
+// GPU outputs be compared with oracle outputs computed elsewhere (host cores, other ranks).
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -76,7 +78,65 @@ __global__ void count_mismatch_kernel(const uint8_t* a, const uint8_t* b, uint64
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
 
+// Per-strip digest (harness, not the method; synthetic/digest.py is the host version):
+//   digest(b) = mix64(len ^ DIGEST_LEN) + sum_k mix64(w_k + k * GOLDEN + DIGEST_DOMAIN)  (mod 2^64)
+// w_k = little-endian u64 of bytes [8k, 8k+8), zero past len.  mix64 is a bijection, so one
+// changed word always changes its term; the sum is order-free, so blocks add their part with
+// one wrapping 64-bit atomic per warp.
+constexpr uint64_t DIGEST_DOMAIN = 0x6A09E667F3BCC909ull;
+constexpr uint64_t DIGEST_LEN = 0xBB67AE8584CAA73Bull;
+constexpr int DIGEST_SEG_WORDS = 4096;  // words per block work unit (32 KiB)
+
+__global__ void digest_init_kernel(unsigned long long* out, uint64_t n, uint64_t len) {
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = mix64(len ^ DIGEST_LEN);
+}
+
+__global__ void digest_kernel(const uint8_t* src, uint64_t strip_stride, uint64_t stripe_stride, uint64_t len,
+                              int nstrips, int nstripes, unsigned long long* out) {
+  const uint64_t wps = (len + 7) / 8;
+  const uint64_t segs = (wps + DIGEST_SEG_WORDS - 1) / DIGEST_SEG_WORDS;
+  const uint64_t units = segs * static_cast<uint64_t>(nstrips) * static_cast<uint64_t>(nstripes);
+  for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const uint64_t strip = u / segs;  // = s * nstrips + t
+    const uint64_t seg = u - strip * segs;
+    const uint64_t s = strip / static_cast<uint64_t>(nstrips), t = strip - s * static_cast<uint64_t>(nstrips);
+    const uint8_t* base = src + s * stripe_stride + t * strip_stride;
+    const bool al8 = (reinterpret_cast<uintptr_t>(base) & 7u) == 0;
+    const uint64_t k0 = seg * DIGEST_SEG_WORDS;
+    const uint64_t k1 = k0 + DIGEST_SEG_WORDS < wps ? k0 + DIGEST_SEG_WORDS : wps;
+    unsigned long long h = 0;
+    for (uint64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+      uint64_t w = 0;
+      if (al8 && 8 * k + 8 <= len) {
+        w = __ldg(reinterpret_cast<const unsigned long long*>(base) + k);
+      } else {
+        for (int b = 0; b < 8; b++)
+          if (8 * k + b < len) w |= static_cast<uint64_t>(__ldg(base + 8 * k + b)) << (8 * b);
+      }
+      h += mix64(w + k * GOLDEN + DIGEST_DOMAIN);
+    }
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out + strip, h);
+  }
+}
+
 }  // namespace
+
+cudaError_t harness_digest(const uint8_t* src, uint64_t strip_stride, uint64_t stripe_stride, uint64_t len,
+                           int nstrips, int nstripes, uint64_t* out, cudaStream_t st) {
+  const uint64_t n = static_cast<uint64_t>(nstrips) * static_cast<uint64_t>(nstripes);
+  auto* o = reinterpret_cast<unsigned long long*>(out);
+  uint64_t ib = (n + 255) / 256;
+  digest_init_kernel<<<static_cast<unsigned>(ib < 1024 ? (ib ? ib : 1) : 1024), 256, 0, st>>>(o, n, len);
+  const uint64_t units = ((len + 7) / 8 + DIGEST_SEG_WORDS - 1) / DIGEST_SEG_WORDS * n;
+  uint64_t blocks = units < 148ull * 8 ? units : 148ull * 8;
+  if (blocks == 0) blocks = 1;
+  digest_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(src, strip_stride, stripe_stride, len, nstrips,
+                                                               nstripes, o);
+  return cudaGetLastError();
+}
 
 cudaError_t harness_fill(uint8_t* dst, uint64_t strip_stride, uint64_t stripe_stride, uint64_t len, int nstrips,
                          int nstripes, uint64_t seed, int cfg, int stripe0, int strip0, int sparse_mode,

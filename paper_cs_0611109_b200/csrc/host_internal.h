@@ -3,6 +3,7 @@
 // xgpu_host.cu: NEXT-4; rs_host.cu: NEXT-3).  Not part of the public ABI (include/raid6c.h).
 #pragma once
 #include <atomic>
+#include <memory>
 #include <cstdint>
 #include <mutex>
 #include <string>
@@ -18,6 +19,8 @@ cudaError_t harness_fill(uint8_t* dst, uint64_t strip_stride, uint64_t stripe_st
                          int nstripes, uint64_t seed, int cfg, int stripe0, int strip0, int sparse_mode,
                          cudaStream_t st);
 cudaError_t harness_count_mismatch(const uint8_t* a, const uint8_t* b, uint64_t len, uint64_t* out, cudaStream_t st);
+cudaError_t harness_digest(const uint8_t* src, uint64_t strip_stride, uint64_t stripe_stride, uint64_t len,
+                           int nstrips, int nstripes, uint64_t* out, cudaStream_t st);
 // NEXT-3 Reed-Solomon baseline (rs.cu)
 const void* rs_kernel_ptr(bool recover);
 size_t rs_smem_bytes(bool recover);
@@ -99,7 +102,7 @@ uint64_t range_granule(raid6c_plan pl);
 raid6c_status upload_erasures(raid6c_plan pl, const raid6c_erasure* er, int count, cudaStream_t st);
 raid6c_status set_erasures(raid6c_plan plan, zp::ZpArgs& a, const raid6c_erasure* erasures, int num_erasures,
                            int erasures_on_device, int num_stripes, bool with_programs);
-raid6c_status cached_plan(int p, int N, size_t bytes, raid6c_plan* out);
+raid6c_status cached_plan(int p, int N, size_t bytes, std::shared_ptr<raid6c_plan_s>* out);
 raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_t stripe_stride, uint8_t* P,
                        uint8_t* Q, size_t parity_stride, int num_stripes, const raid6c_erasure* er, int num_er,
                        bool recover);

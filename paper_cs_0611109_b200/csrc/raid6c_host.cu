@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -554,10 +555,14 @@ raid6c_status set_erasures(raid6c_plan plan, zp::ZpArgs& a, const raid6c_erasure
 }
 
 // ------------------------------------------------------------------ cached single-stripe plans
+// The north-star calls share one plan per (device, p, N, bytes).  Callers hold the plan through
+// a shared_ptr for the whole call, so evicting an entry (the cache is bounded) only drops the
+// cache's reference: a plan is released when its last in-flight call returns, never under it.
 std::mutex g_cache_mu;
-std::map<std::tuple<int, int, int, size_t>, raid6c_plan> g_cache;
+std::map<std::tuple<int, int, int, size_t>, std::shared_ptr<raid6c_plan_s>> g_cache;
+constexpr size_t kCacheMax = 64;
 
-raid6c_status cached_plan(int p, int N, size_t bytes, raid6c_plan* out) {
+raid6c_status cached_plan(int p, int N, size_t bytes, std::shared_ptr<raid6c_plan_s>* out) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) {
     cudaGetLastError();
@@ -571,22 +576,15 @@ raid6c_status cached_plan(int p, int N, size_t bytes, raid6c_plan* out) {
     *out = it->second;
     return RAID6C_OK;
   }
-  raid6c_plan pl = new raid6c_plan_s();
-  raid6c_status st = plan_init(pl, p, N, bytes, dev, nullptr);
-  if (st != RAID6C_OK) {
-    plan_release(pl);
-    delete pl;
-    return st;
-  }
-  if (g_cache.size() > 64) {  // bounded cache
-    for (auto& kv : g_cache) {
-      plan_release(kv.second);
-      delete kv.second;
-    }
-    g_cache.clear();
-  }
+  std::shared_ptr<raid6c_plan_s> pl(new raid6c_plan_s(), [](raid6c_plan_s* q) {
+    plan_release(q);
+    delete q;
+  });
+  raid6c_status st = plan_init(pl.get(), p, N, bytes, dev, nullptr);
+  if (st != RAID6C_OK) return st;  // (the deleter releases what plan_init allocated)
+  if (g_cache.size() >= kCacheMax) g_cache.erase(g_cache.begin());  // one entry; in-use plans live on
   g_cache[key] = pl;
-  *out = pl;
+  *out = std::move(pl);
   return RAID6C_OK;
 }
 
@@ -673,9 +671,10 @@ raid6c_status raid6c_encode(int p, int N, const uint8_t* const* strips, uint8_t*
   if (!strips || !P || !Q) return RAID6C_E_NULL;
   for (int k = 0; k < N; k++)
     if (!strips[k]) return RAID6C_E_NULL;
-  raid6c_plan pl;
-  raid6c_status st = cached_plan(p, N, bytes, &pl);
+  std::shared_ptr<raid6c_plan_s> hold;
+  raid6c_status st = cached_plan(p, N, bytes, &hold);
   if (st != RAID6C_OK) return st;
+  raid6c_plan pl = hold.get();
   zp::ZpArgs a;
   std::memset(&a, 0, sizeof(a));
   for (int k = 0; k < N; k++) a.base[k] = strips[k];
@@ -700,9 +699,10 @@ raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* cons
   if (!strips) return RAID6C_E_NULL;
   for (int k = 0; k < N + 2; k++)
     if (!strips[k]) return RAID6C_E_NULL;
-  raid6c_plan pl;
-  st = cached_plan(p, N, bytes, &pl);
+  std::shared_ptr<raid6c_plan_s> hold;
+  st = cached_plan(p, N, bytes, &hold);
   if (st != RAID6C_OK) return st;
+  raid6c_plan pl = hold.get();
   zp::ZpArgs a;
   std::memset(&a, 0, sizeof(a));
   for (int k = 0; k < N + 2; k++) a.base[k] = strips[k];
@@ -807,6 +807,18 @@ raid6c_status raid6c_count_mismatch(const uint8_t* a, const uint8_t* b, size_t l
   cudaError_t e = zp::harness_count_mismatch(a, b, len, count_dev, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  return RAID6C_OK;
+}
+
+raid6c_status raid6c_digest(const uint8_t* src, size_t strip_stride, size_t stripe_stride, size_t len, int nstrips,
+                            int nstripes, uint64_t* digests_dev, void* stream) {
+  if (!src || !digests_dev) return RAID6C_E_NULL;
+  if (nstrips < 0 || nstripes < 0) return RAID6C_E_SIZE;
+  if (nstrips == 0 || nstripes == 0) return RAID6C_OK;
+  cudaError_t e = zp::harness_digest(src, strip_stride, stripe_stride, len, nstrips, nstripes, digests_dev,
+                                     static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
   return RAID6C_OK;
 }
 

@@ -88,7 +88,11 @@ raid6c_status raid6c_combine_strided(raid6c_plan plan, uint8_t* const* strips, s
     a.src_q[r] = src_q[r];
   }
   const uint64_t gr = range_granule(plan);
-  if (range_lo % gr != 0 || range_hi < range_lo || range_hi > plan->pbytes) return RAID6C_E_SIZE;
+  // both ends on the range grid (or the end of the strip): the kernels work in whole tiles /
+  // groups up to range_hi rounded up, which must not reach into the next owner's range
+  if (range_lo % gr != 0 || range_hi < range_lo || range_hi > plan->pbytes ||
+      (range_hi % gr != 0 && range_hi != plan->pbytes))
+    return RAID6C_E_SIZE;
   if (num_stripes > 1 && part_stride < range_hi - range_lo) return RAID6C_E_SIZE;
   a.nsrc = num_sources;
   a.range_lo = range_lo;

@@ -729,8 +729,19 @@ struct Layout {
   static constexpr int NOUT = num_outputs<MODE>();
   static constexpr int SMEM_TARGET = min_blocks<P, MODE>() == 3 ? 72 * 1024 : 112 * 1024;
   static constexpr int STAGES_RAW = (SMEM_TARGET - NOUT * G::TB - G::MTAB * 8 - 256) / G::TB;
-  static constexpr int STAGES = STAGES_RAW < 3 ? 3 : (STAGES_RAW > 8 ? 8 : STAGES_RAW);
-  static constexpr size_t SMEM = (size_t)(STAGES + NOUT) * G::TB + (size_t)G::MTAB * 8 + 2 * STAGES * 8;
+  static constexpr size_t smem_for(int st) {
+    return (size_t)(st + NOUT) * G::TB + (size_t)G::MTAB * 8 + 2 * st * 8;
+  }
+  static constexpr bool fits(int st) { return (smem_for(st) + 1024) * min_blocks<P, MODE>() <= 228 * 1024; }
+  // at least 3 stages; 2 only where 3 would cost a CTA per SM (large mask tables: p = 233
+  // encode / recovery, the update of p = 73, 137, 241)
+  static constexpr int STAGES = STAGES_RAW >= 3 ? (STAGES_RAW > 8 ? 8 : STAGES_RAW) : (!fits(3) && fits(2) ? 2 : 3);
+  static constexpr size_t SMEM = smem_for(STAGES);
+  // CTAs per SM that the shared memory actually admits (228 KB per SM, 1 KB reserved per CTA);
+  // the launch bounds take this, not the wish of min_blocks (p = 233 update: 1).
+  static constexpr int SMEM_FIT = static_cast<int>((228 * 1024) / (SMEM + 1024));
+  static constexpr int BLOCKS = SMEM_FIT < min_blocks<P, MODE>() ? SMEM_FIT : min_blocks<P, MODE>();
+  static_assert(SMEM <= 227 * 1024 && BLOCKS >= 1, "one CTA must fit the SM's shared memory");
 };
 
 // Per-item epilogue for every mode: fills the NOUT output chunks and their strip indices
@@ -772,7 +783,7 @@ __device__ __forceinline__ void epilogue(const ZpArgs& a, const ItemDesc& d, int
 }
 
 template <int P, int MODE, bool EXT = false>
-__global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (min_blocks<P, MODE>())) zp_kernel(const __grid_constant__ ZpArgs a) {
+__global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>::BLOCKS)) zp_kernel(const __grid_constant__ ZpArgs a) {
   using G = GeoM<P, MODE>;
   using LY = Layout<P, MODE>;
   constexpr int C = G::C, CB = G::CB, TB = G::TB, NT = G::THREADS, ST = LY::STAGES, NOUT = LY::NOUT;

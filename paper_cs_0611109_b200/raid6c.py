@@ -69,6 +69,7 @@ _SIGS = [
     ("raid6c_host_traffic", _i, [_vp, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
     ("raid6c_fill", _i, [_vp, _sz, _sz, _sz, _i, _i, ctypes.c_uint64, _i, _i, _i, _i, _vp]),
     ("raid6c_count_mismatch", _i, [_vp, _vp, _sz, _vp, _vp]),
+    ("raid6c_digest", _i, [_vp, _sz, _sz, _sz, _i, _i, _vp, _vp]),
 ]
 for _name, _res, _args in _SIGS:
     _f = getattr(_lib, _name)
@@ -163,6 +164,14 @@ def fill(dst, strip_stride: int, stripe_stride: int, nbytes: int, nstrips: int, 
 def count_mismatch(a, b, nbytes: int, count_dev, stream=None) -> None:
     _check(_lib.raid6c_count_mismatch(_ptr(a), _ptr(b), nbytes, _ptr(count_dev), _stream_handle(stream)),
            "raid6c_count_mismatch")
+
+
+def digest(src, strip_stride: int, stripe_stride: int, nbytes: int, nstrips: int, nstripes: int, out_dev,
+           stream=None) -> None:
+    """raid6c_digest: out_dev[s*nstrips + t] = 64-bit digest of strip t of stripe s (device int64/uint64
+    tensor of nstrips*nstripes entries; the host definition is synthetic/digest.py)."""
+    _check(_lib.raid6c_digest(_ptr(src), strip_stride, stripe_stride, nbytes, nstrips, nstripes, _ptr(out_dev),
+                              _stream_handle(stream)), "raid6c_digest")
 
 
 # ------------------------------------------------------------------ NEXT-3: RS baseline

@@ -13,9 +13,13 @@ Generator spec:
           else 1 + (uniform byte b % 255).  Draws: bytes 0-3 from mix64(key ^ SPARSE_A),
           bytes 4-7 from mix64(key ^ SPARSE_B), 16 bits each, little-endian.
 mix64 is the SplitMix64 finalizer.
+
+``synthetic.digest`` (a harness comparison tool, also not the method) reduces a strip to a u64;
+the device twin is ``raid6c_digest``.
 """
 from .gen import (GOLDEN, SPARSE_A, SPARSE_B, ERASE_DOMAIN, mix64, strip_bytes,
                   stripe_strips, erasure_pair, all_pairs, pair_class)
+from .digest import digest, combine as combine_digests, length_term, word_terms
 
 __all__ = ["GOLDEN", "SPARSE_A", "SPARSE_B", "ERASE_DOMAIN", "mix64", "strip_bytes",
-           "stripe_strips", "erasure_pair", "all_pairs", "pair_class"]
+           "stripe_strips", "erasure_pair", "all_pairs", "pair_class", "digest", "combine_digests", "length_term", "word_terms"]

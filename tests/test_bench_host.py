@@ -71,3 +71,26 @@ def test_alg_bytes_recover_reads_n_writes_two(cfg, N, nbytes):
     pb = nbytes + 5  # any parity length: the formula is N strips read + 2 strips written per stripe
     pairs = bench.pair_schedule(cfg, N, 10, 0, 0)
     assert bench.alg_bytes_recover(N, nbytes, pb, pairs) == 10 * (N * nbytes + 2 * pb)
+
+
+def test_gpus_n_without_enough_gpus_fails_loudly():
+    """--gpus 2 over NCCL on a box with fewer GPUs must exit non-zero (never run one rank)."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("this check needs a box with fewer than 2 GPUs")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300,
+                       env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert r.returncode == 2 and "needs 2 visible GPUs" in r.stderr
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_world_size_must_match_gpus():
+    import subprocess
+    import sys
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 2 and "3 rank(s) running but --gpus 2" in r.stderr

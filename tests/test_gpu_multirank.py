@@ -1,0 +1,53 @@
+"""bench.py's multi-rank path on the GPU box (one GPU per gpurun call, so the ranks share cuda:0
+under gloo; the kernels of different ranks never wait on each other).
+
+* `bench.py --gpus N` with no torchrun environment brings up N ranks itself and reports
+  n_gpus = N, N per-rank times and N ranks in its line (never one rank silently).
+* Sharding invariance on the GPU: the whole c4 configuration cut into
+  G = 1, 2, 4 block shards gives the same per-strip digests of every strip of the run
+  (verified.digest_all), and each run's oracle digest sample (spread over all shards) matches.
+  Stripes are independent (Eq. (znparity)), so the results cannot depend on G."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _bench(*args, timeout=900):
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), *args]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-3000:]
+    return json.loads(lines[0]), r.stderr
+
+
+def test_self_launch_two_ranks():
+    d, err = _bench("--gpus", "2", "--dist-backend", "gloo", "--config", "2", "--stripes", "8", "--steps", "2",
+                    "--warmup", "3", "--no-e2e", "--oracle-stripes", "4")
+    assert d["n_gpus"] == 2 and len(d["per_rank_ms"]) == 2
+    assert d["ranks"]["ranks_up"] == 2 and [r["rank"] for r in d["ranks"]["ranks"]] == [0, 1]
+    v = d["verified"]
+    assert v["ok"] and v["mismatched_bytes"] == 0 and v["poisoned_recovery"]["mismatched_bytes"] == 0
+    assert v["poisoned_recovery"]["poisoned_bytes"] > 0
+    assert v["oracle_digest_stripes"] == v["oracle_digest_sampled"] == 4
+    assert d["cpu_baseline"]["kind"] == "oracle"
+
+
+@pytest.mark.parametrize("cfg,stripes", [(4, 8)])
+def test_full_config_digests_invariant_to_sharding(cfg, stripes):
+    out = {}
+    for G in (1, 2, 4):
+        d, _ = _bench("--gpus", str(G), "--dist-backend", "gloo", "--full", "--config", str(cfg), "--stripes",
+                      str(stripes), "--warmup", "3", "--oracle-stripes", "4")
+        v = d["verified"]
+        assert d["n_gpus"] == G and v["ok"] and v["scrub_bad_words_after_recovery"] == 0
+        assert v["digested_stripes"] == stripes
+        assert v["oracle_digest_stripes"] == v["oracle_digest_sampled"] == 4
+        out[G] = v["digest_all"]
+    assert out[1] == out[2] == out[4], out

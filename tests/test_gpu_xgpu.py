@@ -150,6 +150,9 @@ def test_xgpu_argument_errors():
         plan.combine_strided(strips, nbytes, nbytes, 1, None, sp, sp, rb, 0, rb)
     with pytest.raises(R.Raid6Error):  # bad erasure index
         plan.combine_strided(strips, nbytes, nbytes, 1, [(0, N + 2)], sp, sp, rb, 0, rb)
+    full = [int(d.data_ptr()) + k * nbytes for k in range(N + 2)]
+    with pytest.raises(R.Raid6Error):  # range end off the granule grid (and not the strip end)
+        plan.combine_strided(full, nbytes, nbytes, 1, None, sp, sp, rb, 0, rb - 16)
 
 
 def test_distributed_ipc_two_processes():
