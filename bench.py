@@ -90,7 +90,7 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for l in self.lines:
             f = [x.strip() for x in l.split(",")]
@@ -99,12 +99,14 @@ class ClockSampler:
             try:
                 sm.append(float(f[1]))
                 mx.append(float(f[2]))
+                pw.append(float(f[3]))
             except ValueError:
                 continue
             for nm, v in zip(names, f[5:9]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "sm_min_mhz": min(sm) if sm else None, "power_w_max": max(pw) if pw else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
@@ -394,11 +396,11 @@ def run_ours(args):
             last = pair_lists[-1]
             dl = [s_ * N + k for s_, pr in enumerate(last) for k in pr if k < N]
             pl = [s_ * 2 + (k - N) for s_, pr in enumerate(last) for k in pr if k >= N]
-            with torch.cuda.stream(stream):
+            with torch.cuda.stream(stream):  # (strip bytes only: the stride padding is not a strip)
                 if dl:
-                    data.view(S * N, ss).index_fill_(0, torch.tensor(dl, device=dev), 0xA5)
+                    data.view(S * N, ss)[:, :nbytes].index_fill_(0, torch.tensor(dl, device=dev), 0xA5)
                 if pl:
-                    par.view(S * 2, ps).index_fill_(0, torch.tensor(pl, device=dev), 0xA5)
+                    par.view(S * 2, ps)[:, :pb].index_fill_(0, torch.tensor(pl, device=dev), 0xA5)
                 plan.recover_strided(*enc_args, pair_dev[-1])
                 R.count_mismatch(data, ref_data, data.numel(), cnt[1:2], stream)
                 R.count_mismatch(par, ref_par, par.numel(), cnt[1:2], stream)
@@ -406,7 +408,7 @@ def run_ours(args):
         if do_enc:
             # (3) a fresh encode over poisoned parity must rewrite P and Q exactly
             with torch.cuda.stream(stream):
-                par.fill_(0xA5)
+                par[:, :, :pb].fill_(0xA5)
                 plan.encode_strided(*enc_args)
                 if do_rec:
                     R.count_mismatch(par, ref_par, par.numel(), cnt[2:3], stream)
@@ -622,6 +624,7 @@ def run_full(args):
     stripe order, so runs at G = 1, 2, 4, 8 can be compared.  value = user bytes of all ranks /
     max-rank sum of the timed kernel intervals (CUDA events on the plan's stream)."""
     import torch
+    import torch.distributed as dist
     import synthetic
     from paper_cs_0611109_b200 import raid6c as R
     from paper_cs_0611109_b200 import shard
@@ -769,7 +772,6 @@ def run_full(args):
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:
-        import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
     if not line["verified"]["ok"]:
@@ -789,6 +791,7 @@ def run_c2_literal(args):
     also rebuilds each of the 91 pairs on one stripe, whose digests must match the GPU's.  Reports
     the per-class recovery GB/s."""
     import torch
+    import torch.distributed as dist
     import synthetic
     from paper_cs_0611109_b200 import raid6c as R
     from paper_cs_0611109_b200 import shard
@@ -937,7 +940,6 @@ def run_c2_literal(args):
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:
-        import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
     if not ok:

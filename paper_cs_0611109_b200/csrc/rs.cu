@@ -228,8 +228,7 @@ __global__ void __launch_bounds__(THREADS + 32, Cfg<RECOVER>::MINB) rs_kernel(co
       mbar_wait(&full[stage], ph);
       ld_chunk_smem<C>(stages + (size_t)stage * TB + tid * CB, L);
       fold(st, a, k, L);
-      __syncwarp();  // release after the loaded lanes are consumed (see zp_fast.cuh)
-      if (lane == 0) mbar_arrive(&empty[stage]);
+      consumer_release(smem_u32(&empty[stage]), lane);  // (proxy fence: see zp_fast.cuh)
       if (++stage == STAGES) { stage = 0; ph ^= 1u; }
     }
     uint32_t o0[C], o1[C];

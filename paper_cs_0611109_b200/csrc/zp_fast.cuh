@@ -60,7 +60,10 @@ constexpr int top_bit(int v) { return v <= 1 ? 0 : 1 + top_bit(v >> 1); }
 // partial: measured +6% on config 1 and +7% for p = 17) and by the NEXT-4 combine (whose word
 // ranges are whole partial tiles), while recovery keeps 48-byte chunks (fewer per-chunk epilogue
 // overheads per byte: C8 measured -10% there).
-template <int P_, bool SMALL8_ = false, int MINLANES_ = 12>
+#ifndef ZP_REC_THREADS
+#define ZP_REC_THREADS 256
+#endif
+template <int P_, bool SMALL8_ = false, int MINLANES_ = 12, bool REC_ = false>
 struct Geo {
   static constexpr int P = P_;
   static constexpr int n = P - 1;
@@ -81,7 +84,7 @@ struct Geo {
   // the 96-register cap spills, measured p = 23 / 47 / 89 encode 0.74-0.82 -> 0.97-1.00 and
   // recovery 0.50-0.56 -> 0.76-0.95 of the copy rate; p = 43: encode 1.05 -> 0.98, recovery 0.74 -> 0.78);
   // not below 20 lanes: 128 threads for p = 73, 97, 113, 137, 193, 241 (12-18 lanes) cost recovery 11-31 %
-  static constexpr int THREADS = SMALL8 ? 256 : (C >= 20 ? 128 : ((32 % n == 0) ? 224 : 256));
+  static constexpr int THREADS = SMALL8 ? 256 : (C >= 20 ? 128 : ((32 % n == 0) ? 224 : (REC_ ? ZP_REC_THREADS : 256)));
   static constexpr int TB = THREADS * CB;            // TMA row (tile) bytes
   static constexpr int MTAB = (n + 1) * LAMBDA;      // mask table entries (uint2)
   static_assert(LAMBDA <= 32, "fast path needs a period of at most 32 lanes");
@@ -110,14 +113,34 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t tx) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// try_wait with a suspend-time hint: the waiting thread sleeps in the barrier unit until the
+// phase completes (or the hint expires) instead of re-polling -- fewer issued instructions on
+// the consumers' waits for TMA data.
+#ifndef ZP_NO_WAIT_HINT
+#define ZP_TRY_WAIT "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 0x989680;\n\t"
+#else  // A/B control: plain try_wait polling
+#define ZP_TRY_WAIT "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
-      "ZP_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "ZP_WAIT_%=:\n\t" ZP_TRY_WAIT
       "@!P1 bra ZP_WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+// The same on a precomputed shared-space address (the consumers' per-row wait and release: no
+// generic-to-shared conversion per row).
+__device__ __forceinline__ void mbar_wait_sa(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "ZP_WAITS_%=:\n\t" ZP_TRY_WAIT
+      "@!P1 bra ZP_WAITS_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_sa(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void tma_load_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -134,6 +157,27 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+// Consumer side of a TMA stage release: this thread's generic-proxy reads of the stage (LDS) are
+// ordered before the async-proxy write (the producer's next cp.async.bulk into the stage) by a
+// proxy fence -- a write-after-read across proxies; the LDS results are otherwise free to land
+// after the arrive, and the compiler may schedule their consumers after it (a long bench run
+// of the r02 fold once came back with 3 KB rebuilt wrong).  __syncwarp then gathers the lanes
+// and lane 0 arrives on the stage's `empty` barrier (count = consumer warps).
+__device__ __forceinline__ void consumer_release(uint32_t empty_bar_sa, int lane) {
+#if defined(ZP_FENCE_LANE0)  // A/B: the warp's reads gathered by __syncwarp, one fence by lane 0
+  __syncwarp();
+  if (lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty_bar_sa) : "memory");
+  }
+#else
+#ifndef ZP_NO_RELEASE_FENCE
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+  __syncwarp();
+  if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty_bar_sa) : "memory");
+#endif
+}
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -268,6 +312,19 @@ __device__ __forceinline__ void rot_dispatch(int key, const uint32_t (&S)[G::C],
   }
 }
 
+// acc += x^a * S for a in [1, p) (no identity check)
+template <class G>
+__device__ __forceinline__ void rot_acc_nz(const uint32_t (&S)[G::C], int a, const uint2* __restrict__ mtab,
+                                           Acc<G>& acc) {
+  if constexpr (G::QMAX == 0 && G::P <= 32) {  // words below 32 bits: no whole-lane shift to dispatch
+    rot_body<G, 0, 0>(S, static_cast<uint32_t>(a), static_cast<uint32_t>(G::P - a), mtab + a * G::LAMBDA, acc);
+  } else {
+    const int q = a >> 5, qp = (G::P - a) >> 5;
+    const uint32_t r = static_cast<uint32_t>(a & 31), rp = static_cast<uint32_t>((G::P - a) & 31);
+    rot_dispatch<G, 0>(q * (G::QMAX + 1) + qp, S, r, rp, mtab + a * G::LAMBDA, acc);
+  }
+}
+
 // acc += x^a * S   (a in [0, p), S reduced or not: only its n stream bits are used)
 template <class G>
 __device__ __forceinline__ void rot_acc(const uint32_t (&S)[G::C], int a, const uint2* __restrict__ mtab, Acc<G>& acc) {
@@ -276,12 +333,13 @@ __device__ __forceinline__ void rot_acc(const uint32_t (&S)[G::C], int a, const 
     for (int l = 0; l < G::C; l++) acc.ay[l] ^= S[l];
     return;
   }
-  const int q = a >> 5, qp = (G::P - a) >> 5;
-  const uint32_t r = static_cast<uint32_t>(a & 31), rp = static_cast<uint32_t>((G::P - a) & 31);
-  rot_dispatch<G, 0>(q * (G::QMAX + 1) + qp, S, r, rp, mtab + a * G::LAMBDA, acc);
+  rot_acc_nz<G>(S, a, mtab, acc);
 }
 
 // V = pi(acc): the reduced n-bit stream of the accumulated R' value.
+// (r02, measured: spreading T by a multiply on the FMA pipe for n < 32, or by per-word sign
+// spreads for n >= 32, instead of the borrow chain -- no serial dependency -- cost c2 recovery
+// 2 % and c5 0.5 %, c4 / c1 unchanged; the chain stays.)
 template <class G>
 __device__ __forceinline__ void reduce(const Acc<G>& acc, uint32_t (&V)[G::C]) {
   constexpr int C = G::C;
@@ -317,11 +375,14 @@ constexpr int NUM_MODES = 6;
 // spill: 1.02 -> 0.83).
 template <int P>
 __host__ __device__ constexpr int recover_min_lanes() {
+#ifdef ZP_REC13_C12  // A/B: 48-byte recovery chunks for p = 13
+  if (P == 13) return 12;
+#endif
   return (P == 7 || P == 13 || P == 17) ? 15 : 12;
 }
 template <int P, int MODE>
 using GeoM = Geo<P, MODE == MODE_ENCODE || MODE == MODE_PARTIAL || MODE == MODE_COMBINE,
-                 MODE == MODE_RECOVER ? recover_min_lanes<P>() : 12>;
+                 MODE == MODE_RECOVER ? recover_min_lanes<P>() : 12, MODE == MODE_RECOVER>;
 constexpr int K_NEW = -1;     // row index of the update's new-data buffer
 constexpr int K_PART_P = -2;  // partial-mode outputs (slots of the word-range owners)
 constexpr int K_PART_Q = -3;
@@ -471,6 +532,64 @@ __device__ __forceinline__ void fold_row(const ZpArgs& a, const ItemDesc& d, int
       if (amt < 0) amt += G::P;
       rot_acc<G>(L, amt, mtab, acc);
     }
+  }
+}
+
+// The consumer side of one body item of encode / recovery (basic code), row by row in the
+// producer's order: the data strips k < N without the lost pair, then P, then Q (each if it
+// survives).  Data rows feed P and Q, P feeds P, Q feeds Q; the rotation amount
+// (k - base) mod p is carried from strip to strip (Q's is (p - base) mod p = the amount of
+// k = 0), so the per-row work is the wait, the chunk load, the fold and the release only.
+template <class G, int ST>
+__device__ __forceinline__ void fold_item(const ZpArgs& a, const ItemDesc& d, const uint8_t* my_stages,
+                                          uint32_t full_sa, uint32_t empty_sa, const uint2* __restrict__ mtab,
+                                          int lane, uint32_t& stage, uint32_t& ph, uint32_t (&Pa)[G::C],
+                                          Acc<G>& acc) {
+  constexpr int C = G::C;
+  auto next_row = [&](uint32_t (&L)[C]) {
+    mbar_wait_sa(full_sa + 8u * stage, ph);
+    ld_chunk_smem<C>(my_stages + static_cast<size_t>(stage) * G::TB, L);
+  };
+  auto release = [&]() {
+    consumer_release(empty_sa + 8u * stage, lane);
+    if (++stage == ST) { stage = 0; ph ^= 1u; }
+  };
+  const int amt0 = d.base == 0 ? 0 : G::P - d.base;  // (0 - base) mod p
+  int amt = amt0, k = 0;
+  if (amt0 == 0) {  // base 0 (encode, PQ, DQ): strip 0 (if it survives) enters Q as x^0 d_0
+    if (d.x != 0) {
+      uint32_t L[C];
+      next_row(L);
+#pragma unroll
+      for (int l = 0; l < C; l++) { Pa[l] ^= L[l]; acc.ay[l] ^= L[l]; }
+      release();
+    }
+    k = amt = 1;
+  }
+  // from here amt != 0 on every surviving strip: it is 0 only at k = base, a lost strip
+  for (; k < a.N; k++) {
+    if (k != d.x && k != d.y) {
+      uint32_t L[C];
+      next_row(L);
+#pragma unroll
+      for (int l = 0; l < C; l++) Pa[l] ^= L[l];
+      rot_acc_nz<G>(L, amt, mtab, acc);
+      release();
+    }
+    amt = amt + 1 == G::P ? 0 : amt + 1;
+  }
+  if (d.x != a.N && d.y != a.N) {  // P
+    uint32_t L[C];
+    next_row(L);
+#pragma unroll
+    for (int l = 0; l < C; l++) Pa[l] ^= L[l];
+    release();
+  }
+  if (d.y != a.N + 1) {  // Q
+    uint32_t L[C];
+    next_row(L);
+    rot_acc<G>(L, amt0, mtab, acc);
+    release();
   }
 }
 
@@ -841,6 +960,8 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
 
   // -------------------------------------------------- consumers: body tiles via the pipeline
   uint32_t stage = 0, ph = 0;
+  const uint8_t* my_stages = stages + tid * CB;
+  const uint32_t full_sa = smem_u32(full), empty_sa = smem_u32(empty);
   for (uint64_t it = blockIdx.x; it < body_items; it += gridDim.x) {
     const int s = static_cast<int>(it / tiles);
     const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
@@ -856,6 +977,11 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
       if (tid == 0) bulk_wait_read0();
       named_bar_sync(1, NT);
     }
+    // (words that straddle lanes; for lane-aligned words, n | 32, the generic row loop measured
+    // faster: c1 encode / recovery -5 / -8 % with fold_item)
+    if constexpr ((MODE == MODE_ENCODE || MODE == MODE_RECOVER) && !EXT && (32 % G::n != 0)) {
+      fold_item<G, ST>(a, d, my_stages, full_sa, empty_sa, mtab, lane, stage, ph, Pa, acc);
+    } else
     for (int r = 0; r < R; r++) {
       uint32_t L[C];
       mbar_wait(&full[stage], ph);
@@ -872,16 +998,15 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
         }
         fold_row<G, EXT>(a, d, k, L, mtab, Pa, acc);
       }
-      // Release the stage only after every loaded lane has been consumed: an mbarrier.arrive
-      // issued right after the LDS does not wait for the loads to complete, and the producer's
-      // next TMA write (async proxy) can then overwrite the row under a lagging warp's reads.
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
+      consumer_release(empty_sa + 8u * stage, lane);
       if (++stage == ST) { stage = 0; ph ^= 1u; }
     }
     uint32_t o0[C], o1[C];
     int k0 = 0, k1 = 0, k2 = 0;
     epilogue<EMODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+#ifdef ZP_NOOP_RECOVER  // negative control of bench.py's verification: recovery stores nothing
+    if constexpr (MODE == MODE_RECOVER) continue;
+#endif
     if constexpr (NOUT > 0) {
       if constexpr (MODE != MODE_UPDATE) {  // (update waited at the start of the item)
         if (tid == 0) bulk_wait_read0();  // previous item's bulk stores have read outb
@@ -952,6 +1077,9 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
       epilogue<MODE, G, false, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
     } else {
       epilogue<EMODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
+#ifdef ZP_NOOP_RECOVER
+      if constexpr (MODE == MODE_RECOVER) continue;
+#endif
       st_chunk_global<C>(out_ptr(a, k0, s, off), off, row_len(a, k0), o0);
       st_chunk_global<C>(out_ptr(a, k1, s, off), off, row_len(a, k1), o1);
     }

@@ -540,3 +540,31 @@ def test_generic_prime_encode_recover_scrub(p):
         for k in range(N):
             assert np.array_equal(b.numpy_strip(s, k), data[k]), (p, s, k)
         assert np.array_equal(b.numpy_strip(s, N), P) and np.array_equal(b.numpy_strip(s, N + 1), Q), (p, s)
+
+
+# ------------------------------------------------------------------ long-run pipeline check
+@pytest.mark.parametrize("p,N,nbytes,S,launches", [(13, 12, 4 << 20, 256, 400), (61, 60, 32 << 20, 8, 200)])
+def test_long_run_round_trip(p, N, nbytes, S, launches):
+    """bench.py's resident batch driven for hundreds of back-to-back launches (encode, then a
+    recovery of a different pair in every stripe, repeated), the round trip checked every 20
+    launches: a stage released before its reads completed (a TMA refill racing the consumers)
+    shows up here as bytes that stop matching.  c2 at full size; c5 strips, 8 stripes."""
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=0, cfg=2 if p == 13 else 5)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    ref_d, ref_p = b.data.clone(), b.par.clone()
+    allp = synthetic.all_pairs(N)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    pairs = [torch.tensor([allp[(s + 37 * t) % len(allp)] for s in range(S)], dtype=torch.int32, device="cuda")
+             for t in range(launches // 2)]
+    for t in range(launches // 2):
+        plan.encode_strided(*b.args())
+        plan.recover_strided(*b.args(), pairs[t])
+        if t % 10 == 9:
+            plan.sync()
+            R.count_mismatch(b.data, ref_d, b.data.numel(), cnt)
+            R.count_mismatch(b.par, ref_p, b.par.numel(), cnt)
+            torch.cuda.synchronize()
+            assert int(cnt.item()) == 0, f"mismatch after {2 * (t + 1)} launches"
