@@ -51,6 +51,16 @@ const FastEntry* fast_entry_241();
 const FastEntry* fast_entry_257();
 
 const FastEntry* fast_entry(int p) {
+#ifdef ZP_SLIM  // A/B variant libraries (tools/build_variant.py --slim): the configs' primes only
+  switch (p) {
+    case 5: return fast_entry_5();
+    case 13: return fast_entry_13();
+    case 59: return fast_entry_59();
+    case 61: return fast_entry_61();
+    case 257: return fast_entry_257();
+    default: return nullptr;
+  }
+#endif
   switch (p) {
     case 3: return fast_entry_3();
     case 5: return fast_entry_5();

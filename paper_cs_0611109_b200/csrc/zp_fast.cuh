@@ -359,6 +359,27 @@ __device__ __forceinline__ void reduce(const Acc<G>& acc, uint32_t (&V)[G::C]) {
   for (int l = 0; l < C; l++) V[l] = (acc.ax[l] & ~m0_mask<G::n>(l % G::LAMBDA)) ^ acc.ay[l] ^ F[l];
 }
 
+// V = pi(acc) + E for a reduced E (the DD syndrome t = dP + x^{-x} dQ): E rides in the last
+// three-input XOR of the reduction instead of a separate pass over the accumulator.
+template <class G>
+__device__ __forceinline__ void reduce_plus(const Acc<G>& acc, const uint32_t (&E)[G::C], uint32_t (&V)[G::C]) {
+  constexpr int C = G::C;
+  constexpr int qn = G::n >> 5, rn = G::n & 31;
+  uint32_t T[C + 1], Ts[C + 1], F[C + 1];
+#pragma unroll
+  for (int l = 0; l < C; l++) T[l] = acc.ax[l] & m0_mask<G::n>(l % G::LAMBDA);
+  T[C] = acc.tc & 1u;
+#pragma unroll
+  for (int l = 0; l <= C; l++) {
+    const uint32_t lo = (l + qn <= C) ? T[l + qn <= C ? l + qn : 0] : 0u;
+    const uint32_t hi = (l + qn + 1 <= C) ? T[l + qn + 1 <= C ? l + qn + 1 : 0] : 0u;
+    Ts[l] = rn ? __funnelshift_r(lo, hi, rn) : lo;
+  }
+  SubChain<C + 1>::run(F, T, Ts);
+#pragma unroll
+  for (int l = 0; l < C; l++) V[l] = (acc.ax[l] & ~m0_mask<G::n>(l % G::LAMBDA)) ^ acc.ay[l] ^ (F[l] ^ E[l]);
+}
+
 // ------------------------------------------------------------------ stripe bookkeeping
 enum : int { CLS_PQ = 0, CLS_DQ = 1, CLS_DP = 2, CLS_DD = 3, CLS_SCRUB = 4, CLS_UPDATE = 5 };
 // Kernel modes (compile-time): the method's two operations and the NEXT-1 pair around them.
@@ -651,6 +672,58 @@ struct SeriesPlan {
 // (reading R11) with b = x^{bz}, bz = 2z, times x^{e0}.  The evaluation
 // order is chosen at compile time (SeriesPlan): direct, two-level, or doubling chain; e0 is
 // folded into the rotation amounts of the first level (the chain pays one rotation for it).
+// Basic-code form (e0 = 0): every rotation amount bz*j mod p is nonzero (p prime, bz != 0), and
+// each level's x^0 term is peeled out of the runtime loop, so it initialises the accumulator
+// (no zeroing pass, no identity-rotation branch).
+template <class G>
+__device__ __forceinline__ void series_apply0(const uint32_t (&t)[G::C], int bz, const uint2* __restrict__ mtab,
+                                              Acc<G>& acc, uint32_t (&out)[G::C]) {
+  constexpr int C = G::C;
+  constexpr int M = (G::P + 1) / 2;
+  constexpr int TOP = top_bit(M);
+  using SP = SeriesPlan<M>;
+  auto start = [&](const uint32_t (&B)[C]) {  // acc = B (the x^0 term)
+#pragma unroll
+    for (int l = 0; l < C; l++) { acc.ax[l] = 0u; acc.ay[l] = B[l]; }
+    acc.tc = 0u;
+  };
+  if constexpr (!SP::CHAIN) {
+    // two-level: S = sum_{i<M1} b^{i M2} T + sum_{m=M1 M2}^{M-1} b^m t, T = sum_{j<M2} b^j t
+    uint32_t T[C];
+    start(t);
+#pragma unroll 1
+    for (int j = 1; j < SP::M2; j++) rot_acc_nz<G>(t, (bz * j) % G::P, mtab, acc);
+    if constexpr (SP::M2 == M) {
+      reduce<G>(acc, out);
+    } else {
+      reduce<G>(acc, T);
+      start(T);
+#pragma unroll 1
+      for (int i = 1; i < SP::M1; i++) rot_acc_nz<G>(T, (bz * SP::M2 * i) % G::P, mtab, acc);
+#pragma unroll 1
+      for (int m = SP::M1 * SP::M2; m < M; m++) rot_acc_nz<G>(t, (bz * m) % G::P, mtab, acc);
+      reduce<G>(acc, out);
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < C; l++) out[l] = t[l];  // S_1 = t
+    int m = 1;
+#pragma unroll 1
+    for (int bit = TOP - 1; bit >= 0; bit--) {
+      start(out);  // S_{2m} = S_m + b^m S_m
+      rot_acc_nz<G>(out, (bz * m) % G::P, mtab, acc);
+      reduce<G>(acc, out);
+      m *= 2;
+      if ((M >> bit) & 1) {  // S_{m+1} = S_m + b^m t
+        start(out);
+        rot_acc_nz<G>(t, (bz * m) % G::P, mtab, acc);
+        reduce<G>(acc, out);
+        m += 1;
+      }
+    }
+  }
+}
+
 template <class G>
 __device__ __forceinline__ void series_apply(const uint32_t (&t)[G::C], int bz, int e0,
                                              const uint2* __restrict__ mtab, Acc<G>& acc, uint32_t (&out)[G::C]) {
@@ -794,12 +867,10 @@ __device__ __forceinline__ void finish(const ZpArgs& a, const ItemDesc& d, uint3
     for (int l = 0; l < C; l++) o1[l] = Pa[l] ^ o0[l];
     k0 = d.x; k1 = a.N;
   } else {  // DD: d_y = (1+x^z)^{-1}(dP + x^{-x} dQ), d_x = d_y + dP
-#pragma unroll
-    for (int l = 0; l < C; l++) acc.ay[l] ^= Pa[l];
     uint32_t t[C];
-    reduce<G>(acc, t);
+    reduce_plus<G>(acc, Pa, t);
     // d_y = S_M t with S_M = sum_{m<M} b^m, b = x^{2z}, M = (p+1)/2 (reading R11)
-    series_apply<G>(t, (2 * (d.y - d.x)) % G::P, 0, mtab, acc, o1);
+    series_apply0<G>(t, (2 * (d.y - d.x)) % G::P, mtab, acc, o1);
 #pragma unroll
     for (int l = 0; l < C; l++) o0[l] = o1[l] ^ Pa[l];
     k0 = d.x; k1 = d.y;
