@@ -164,19 +164,11 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // of the r02 fold once came back with 3 KB rebuilt wrong).  __syncwarp then gathers the lanes
 // and lane 0 arrives on the stage's `empty` barrier (count = consumer warps).
 __device__ __forceinline__ void consumer_release(uint32_t empty_bar_sa, int lane) {
-#if defined(ZP_FENCE_LANE0)  // A/B: the warp's reads gathered by __syncwarp, one fence by lane 0
-  __syncwarp();
-  if (lane == 0) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty_bar_sa) : "memory");
-  }
-#else
-#ifndef ZP_NO_RELEASE_FENCE
+#ifndef ZP_NO_RELEASE_FENCE  // (negative control only)
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #endif
   __syncwarp();
   if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty_bar_sa) : "memory");
-#endif
 }
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -396,9 +388,6 @@ constexpr int NUM_MODES = 6;
 // spill: 1.02 -> 0.83).
 template <int P>
 __host__ __device__ constexpr int recover_min_lanes() {
-#ifdef ZP_REC13_C12  // A/B: 48-byte recovery chunks for p = 13
-  if (P == 13) return 12;
-#endif
   return (P == 7 || P == 13 || P == 17) ? 15 : 12;
 }
 template <int P, int MODE>
