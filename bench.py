@@ -410,14 +410,13 @@ def run_ours(args):
             with torch.cuda.stream(stream):
                 par[:, :, :pb].fill_(0xA5)
                 plan.encode_strided(*enc_args)
-                if do_rec:
-                    R.count_mismatch(par, ref_par, par.numel(), cnt[2:3], stream)
+                R.count_mismatch(par, ref_par, par.numel(), cnt[2:3], stream)
         stream.synchronize()
         mism = [int(v) for v in cnt.tolist()]
         tot = shard.sum_over_ranks(mism + [2 * data.numel() if do_rec else 0, poisoned], dev)
         verified = {"mismatched_bytes": tot[0], "checked_bytes": tot[3],
                     "poisoned_recovery": {"poisoned_bytes": tot[4], "mismatched_bytes": tot[1]} if do_rec else None,
-                    "fresh_encode_mismatched_bytes": tot[2] if (do_enc and do_rec) else None}
+                    "fresh_encode_mismatched_bytes": tot[2] if do_enc else None}
         # (4) per-strip digests of every stripe (GPU), gathered; the oracle sample below checks them
         if not rs:
             dg = gpu_strip_digests(R, torch, data, par, S, N, ss, ps, nbytes, pb, stream, dev)
@@ -1117,7 +1116,7 @@ def run_sweep(args):
     for k in range(9):
         b = (64 << 10) << k
         cmd = [sys.executable, os.path.abspath(__file__), "--config", "3", "--strip-bytes", str(b),
-               "--steps", str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--no-cpu-baseline"]
+               "--steps", str(args.steps), "--warmup", str(args.warmup), "--no-e2e", "--oracle-stripes", "2"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise SystemExit(f"sweep point {b} failed:\n{r.stderr[-2000:]}")
@@ -1125,7 +1124,8 @@ def run_sweep(args):
         kk = d["kernels"]["encode"]
         pts.append({"strip_bytes": b, "stripes": d["config"]["stripes_per_gpu"], "user_GBps": kk["user_GBps"],
                     "achieved_GBps": kk["achieved_GBps"], "frac_of_peak": kk["frac_of_peak"],
-                    "avg_ms": kk["avg_ms"], "verified_oracle": d["verified"]["oracle_segments_match"],
+                    "avg_ms": kk["avg_ms"], "verified": d["verified"]["ok"],
+                    "oracle_digest_stripes": d["verified"].get("oracle_digest_stripes"),
                     "clocks": d["clocks"]})
     peak, peak_src = measured_peak()
     best = max(pts, key=lambda q: q["achieved_GBps"])

@@ -345,6 +345,15 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
       a.body_tiles = aligned ? pl->bytes / TB : 0;
       const uint64_t body_end = a.body_tiles * TB;
       a.tail_units_per_stripe = (pl->pbytes - body_end + CB - 1) / CB;
+      a.last_tile = 0;
+      // a short strip end through one partial TMA tile (kernels that support it; every row of
+      // the stripe then has the same length and the rest is a multiple of 16 bytes)
+      const uint64_t rest = pl->pbytes - body_end;
+      if (aligned && !pl->ext && fe->partial_tile[mode] && pl->pbytes == pl->bytes && rest > 0 && rest % 16 == 0) {
+        a.body_tiles += 1;
+        a.last_tile = static_cast<uint32_t>(rest);
+        a.tail_units_per_stripe = 0;
+      }
     }
     const uint64_t items = a.body_tiles * static_cast<uint64_t>(a.num_stripes);
     const uint64_t tail_ctas =

@@ -38,6 +38,9 @@ struct ZpArgs {
   //   tail: bytes [body_tiles*TB, pbytes) via direct loads, chunk_bytes per unit.
   uint64_t body_tiles;
   uint64_t tail_units_per_stripe;
+  // != 0: the last body tile of every strip is partial -- this many bytes (a multiple of 16;
+  // kernels with FastEntry::partial_tile only, all rows then being `bytes` long)
+  uint32_t last_tile;
   // NEXT-1 modes.  update: strip upd[s*upd_stride] (or upd_k) of stripe s is rewritten with
   // the new data at nbase + s*new_stride; scrub: counts[s] += words violating a parity equation.
   const int32_t* upd;
@@ -78,6 +81,7 @@ struct FastEntry {
   // __global__ void(ZpArgs) per mode: encode, recover, scrub, update, partial, combine (NEXT-4)
   const void* kernel[6];
   size_t smem_bytes[6];
+  int partial_tile[6];  // the mode's kernel loads / stores a partial last tile through TMA
   const void* kernel_ext[6];  // extended-code (N > p) kernels, nullptr if p fails Theorem 25.3
   size_t smem_ext[6];
 };

@@ -923,6 +923,19 @@ struct Layout {
   static_assert(SMEM <= 227 * 1024 && BLOCKS >= 1, "one CTA must fit the SM's shared memory");
 };
 
+// Kernels that finish a short strip end with a partial TMA tile (ZpArgs::last_tile): encode and
+// recovery of lane-aligned words (n | 32: p = 3, 5, 17 -- config 1's 64 KiB strips leave 1 KiB
+// after the last whole tile).  Other kernels keep the direct tail path: r01 measured the partial
+// tile in every kernel at -3..6 % elsewhere (code size), so it is compiled in only here.
+template <int P, int MODE, bool EXT>
+__host__ __device__ constexpr bool has_partial_tile() {
+#ifdef ZP_NO_PARTIAL_TILE  // A/B control
+  return false;
+#else
+  return (32 % (P - 1) == 0) && (MODE == MODE_ENCODE || MODE == MODE_RECOVER) && !EXT;
+#endif
+}
+
 // Per-item epilogue for every mode: fills the NOUT output chunks and their strip indices
 // (scrub: adds the count of words violating a parity equation to a.counts[s]).
 template <int MODE, class G, bool WARP_UNIFORM = true, bool EXT = false>
@@ -992,6 +1005,14 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
 
   const uint64_t tiles = a.body_tiles;
   const uint64_t body_items = tiles * static_cast<uint64_t>(a.num_stripes);
+  // A strip length that leaves less than a tile (c1: 1 KiB of every 64 KiB strip) is finished by
+  // one partial TMA tile when the kernel supports it (lane-aligned words, encode / recovery);
+  // its chunks past the data compute on stale stage bytes that are never stored.
+  constexpr bool PART = has_partial_tile<P, MODE, EXT>();
+  auto tile_len = [&](uint64_t t) -> uint32_t {
+    if constexpr (PART) return (a.last_tile != 0u && t + 1 == tiles) ? a.last_tile : static_cast<uint32_t>(TB);
+    return static_cast<uint32_t>(TB);
+  };
 
   if (warp == NT / 32) {
     // ------------------------------------------------ producer: one lane issues all TMA rows
@@ -1004,13 +1025,14 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
         const int R = num_rows<MODE>(a, d);
         for (int r = 0; r < R; r++) {
           const uint8_t* g = in_ptr<MODE>(a, r, d, s, t * TB);
+          const uint32_t len = tile_len(t);
           // the whole row tile lies inside its strip (combine: inside the slot's range)
-          ZP_CHECK((t + 1) * TB <= (MODE == MODE_COMBINE ? a.range_hi - a.range_lo
-                                                           : row_len(a, row_strip<MODE>(a, r, d))));
-          ZP_CHECK((reinterpret_cast<uintptr_t>(g) & 15u) == 0);
+          ZP_CHECK(t * TB + len <= (MODE == MODE_COMBINE ? a.range_hi - a.range_lo
+                                                         : row_len(a, row_strip<MODE>(a, r, d))));
+          ZP_CHECK((reinterpret_cast<uintptr_t>(g) & 15u) == 0 && len % 16 == 0);
           mbar_wait(&empty[stage], ph ^ 1u);
-          mbar_expect_tx(&full[stage], TB);
-          tma_load_row(stages + (size_t)stage * TB, g, TB, &full[stage]);
+          mbar_expect_tx(&full[stage], len);
+          tma_load_row(stages + (size_t)stage * TB, g, len, &full[stage]);
           if (++stage == ST) { stage = 0; ph ^= 1u; }
         }
       }
@@ -1078,15 +1100,16 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
       named_bar_sync(1, NT);
       if (tid == 0) {
         const uint64_t ob = obase + t * TB;
+        const uint32_t len = tile_len(t);
         // every stored tile lies inside its output strip (partial: inside one owner's slot)
-        ZP_CHECK(ob + TB <= row_len(a, k0) && ob + TB <= row_len(a, k1));
-        if constexpr (NOUT == 3) ZP_CHECK(ob + TB <= row_len(a, k2));
+        ZP_CHECK(ob + len <= row_len(a, k0) && ob + len <= row_len(a, k1));
+        if constexpr (NOUT == 3) ZP_CHECK(ob + len <= row_len(a, k2));
         if constexpr (MODE == MODE_PARTIAL)
           ZP_CHECK(ob / a.range_bytes < static_cast<uint64_t>(a.nranges) &&
                    ob % a.range_bytes + TB <= a.range_bytes);
-        tma_store_row(out_ptr(a, k0, s, ob), outb, TB);
-        tma_store_row(out_ptr(a, k1, s, ob), outb + TB, TB);
-        if constexpr (NOUT == 3) tma_store_row(out_ptr(a, k2, s, ob), outb + 2 * TB, TB);
+        tma_store_row(out_ptr(a, k0, s, ob), outb, len);
+        tma_store_row(out_ptr(a, k1, s, ob), outb + TB, len);
+        if constexpr (NOUT == 3) tma_store_row(out_ptr(a, k2, s, ob), outb + 2 * TB, len);
         bulk_commit();
       }
     }
@@ -1155,6 +1178,7 @@ void fill_geo(FastEntry& e) {
     e.chunk_bytes[M] = G::CB;
     e.tile_bytes[M] = G::TB;
     e.threads[M] = G::THREADS;
+    e.partial_tile[M] = has_partial_tile<P, M, false>() ? 1 : 0;
     fill_geo<P, M + 1>(e);
   }
 }

@@ -25,6 +25,9 @@ for op in update scrub; do for c in 1 2 3 4 5; do run next1_${op}_c$c 600 --conf
 for spec in "2 25" "2 17" "4 115" "5 121" "3 300" "1 9"; do set -- $spec; run next2_c$1_N$2 600 --config $1 --data-strips $2 --no-e2e --no-cpu-baseline; done
 for spec in "4 8" "5 8" "2 4" "2 8" "1 4" "3 8"; do set -- $spec; run next4_xgpu_c$1_G$2 600 --config $1 --xgpu $2; done
 for p in 233 241 137 73; do run prime_p$p 600 --config 2 --prime $p --no-e2e --no-cpu-baseline --steps 5; done
+# the same primes on the round-1 library (ADVICE: p = 233's shared memory admitted 1 CTA per SM)
+if [ -f build/var/libB.so ]; then for p in 233 241 137 73; do RAID6C_LIB=$PWD/build/var/libB.so run prime_r01_p$p 600 --config 2 --prime $p --no-e2e --no-cpu-baseline --steps 5; done; fi
+for p in 233 73; do run update_p$p 600 --config 2 --prime $p --op update; done
 run impl_reference 600 --impl reference
 # ncu: launch list of the default workload (2 timed steps) and full-set captures (c2 encode + recover, c1)
 B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
