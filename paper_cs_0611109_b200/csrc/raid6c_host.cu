@@ -349,7 +349,14 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
       // a short strip end through one partial TMA tile (kernels that support it; every row of
       // the stripe then has the same length and the rest is a multiple of 16 bytes)
       const uint64_t rest = pl->pbytes - body_end;
-      if (aligned && !pl->ext && fe->partial_tile[mode] && pl->pbytes == pl->bytes && rest > 0 && rest % 16 == 0) {
+      // recovery takes it only in small launches (fewer items than resident CTAs): there the
+      // direct tail path is the latency (config 1 literally: 22 -> 18 us per call), while in a
+      // large launch a partial item costs a whole item's solve for a sliver of the data (c1
+      // batched: -4.5 %); encode always (c1 batched +1.3 %)
+      const bool small = (a.body_tiles + 1) * static_cast<uint64_t>(a.num_stripes) <=
+                         static_cast<uint64_t>(pl->num_sms) * pl->occ[mode];
+      if (aligned && !pl->ext && fe->partial_tile[mode] && pl->pbytes == pl->bytes && rest > 0 && rest % 16 == 0 &&
+          (mode == zp::KMODE_ENCODE || small)) {
         a.body_tiles += 1;
         a.last_tile = static_cast<uint32_t>(rest);
         a.tail_units_per_stripe = 0;

@@ -603,6 +603,52 @@ __device__ __forceinline__ void fold_item(const ZpArgs& a, const ItemDesc& d, co
   }
 }
 
+// The same walk for the extended code (Eq. (qext), NEXT-2): rotation origin 0, data strip k
+// enters Q as x^k (k < p) or (1 + x^{k-p+1}) (k >= p; k-p+1 in [1, p-1]), Q as itself.
+template <class G, int ST>
+__device__ __forceinline__ void fold_item_ext(const ZpArgs& a, const ItemDesc& d, const uint8_t* my_stages,
+                                              uint32_t full_sa, uint32_t empty_sa, const uint2* __restrict__ mtab,
+                                              int lane, uint32_t& stage, uint32_t& ph, uint32_t (&Pa)[G::C],
+                                              Acc<G>& acc) {
+  constexpr int C = G::C;
+  auto next_row = [&](uint32_t (&L)[C]) {
+    mbar_wait_sa(full_sa + 8u * stage, ph);
+    ld_chunk_smem<C>(my_stages + static_cast<size_t>(stage) * G::TB, L);
+  };
+  auto release = [&]() {
+    consumer_release(empty_sa + 8u * stage, lane);
+    if (++stage == ST) { stage = 0; ph ^= 1u; }
+  };
+  for (int k = 0; k < a.N; k++) {
+    if (k == d.x || k == d.y) continue;
+    uint32_t L[C];
+    next_row(L);
+    if (k == 0 || k >= G::P) {
+#pragma unroll
+      for (int l = 0; l < C; l++) { Pa[l] ^= L[l]; acc.ay[l] ^= L[l]; }
+    } else {
+#pragma unroll
+      for (int l = 0; l < C; l++) Pa[l] ^= L[l];
+    }
+    if (k != 0) rot_acc_nz<G>(L, k < G::P ? k : k - G::P + 1, mtab, acc);
+    release();
+  }
+  if (d.x != a.N && d.y != a.N) {  // P
+    uint32_t L[C];
+    next_row(L);
+#pragma unroll
+    for (int l = 0; l < C; l++) Pa[l] ^= L[l];
+    release();
+  }
+  if (d.y != a.N + 1) {  // Q
+    uint32_t L[C];
+    next_row(L);
+#pragma unroll
+    for (int l = 0; l < C; l++) acc.ay[l] ^= L[l];
+    release();
+  }
+}
+
 // Combine fold: row 2r is source r's dP part, row 2r+1 its dQ part (reduced words: rotation 0).
 template <class G>
 __device__ __forceinline__ void fold_partial(int r, const uint32_t (&L)[G::C], uint32_t (&Pa)[G::C], Acc<G>& acc) {
@@ -1063,6 +1109,8 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
     // faster: c1 encode / recovery -5 / -8 % with fold_item)
     if constexpr ((MODE == MODE_ENCODE || MODE == MODE_RECOVER) && !EXT && (32 % G::n != 0)) {
       fold_item<G, ST>(a, d, my_stages, full_sa, empty_sa, mtab, lane, stage, ph, Pa, acc);
+    } else if constexpr ((MODE == MODE_ENCODE || MODE == MODE_RECOVER) && EXT && (32 % G::n != 0)) {
+      fold_item_ext<G, ST>(a, d, my_stages, full_sa, empty_sa, mtab, lane, stage, ph, Pa, acc);
     } else
     for (int r = 0; r < R; r++) {
       uint32_t L[C];

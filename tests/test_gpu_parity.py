@@ -573,31 +573,33 @@ def test_long_run_round_trip(p, N, nbytes, S, launches):
 # ------------------------------------------------------------------ partial last TMA tile
 @pytest.mark.parametrize("p,N", [(3, 2), (5, 4), (17, 16)])
 @pytest.mark.parametrize("rest", [16, 1024, 7152])
-def test_partial_last_tile(p, N, rest):
+@pytest.mark.parametrize("S", [2, 600])
+def test_partial_last_tile(p, N, rest, S):
     """Lane-aligned words (n | 32) finish a strip whose length leaves `rest` bytes after the
     last whole tile with one partial TMA tile (encode / recovery kernels, ZpArgs::last_tile).
     Strips of 3 whole tiles + rest bytes (rest a multiple of 16) in a persistent launch: every
     stripe's P/Q equal the oracle, and every erasure class rebuilds the whole strips, with the
-    guard bytes past each strip untouched."""
+    guard bytes past each strip untouched.  S = 600: a persistent launch (recovery then keeps the
+    direct tail path); S = 2: a small launch (recovery takes the partial tile too)."""
     nbytes = 3 * 10752 + rest if rest < 10752 else rest
-    S = 600  # more items than CTAs
     b = Batch(p, N, nbytes, S, align=0)
     assert b.pb == nbytes
     b.fill_synthetic(seed=0, cfg=1)
     plan = R.Plan(p, N, nbytes)
     plan.encode_strided(*b.args())
     plan.sync()
-    for s in (0, 1, S - 1):
+    for s in sorted({0, 1, S - 1}):
         data = synthetic.stripe_strips(0, 1, s, N, nbytes)
         P, Q = oracle.encode(p, data, nbytes)
         assert np.array_equal(_np(b.strip(s, N)), P) and np.array_equal(_np(b.strip(s, N + 1)), Q), s
     allp = synthetic.all_pairs(N)
     ref_d, ref_p = b.data.clone(), b.par.clone()
     guard_d, guard_p = b.dbuf[-64:].clone(), b.pbuf[-64:].clone()
-    pairs = [allp[s % len(allp)] for s in range(S)]
-    for s, pr in enumerate(pairs):
-        _poison(b, s, pr)
-    plan.recover_strided(*b.args(), torch.tensor(pairs, dtype=torch.int32, device="cuda"))
-    plan.sync()
-    assert torch.equal(b.data, ref_d) and torch.equal(b.par, ref_p)
-    assert torch.equal(b.dbuf[-64:], guard_d) and torch.equal(b.pbuf[-64:], guard_p)
+    for r in range(len(allp) if S == 2 else 1):  # small launches: every pair
+        pairs = [allp[(s + r) % len(allp)] for s in range(S)]
+        for s, pr in enumerate(pairs):
+            _poison(b, s, pr)
+        plan.recover_strided(*b.args(), torch.tensor(pairs, dtype=torch.int32, device="cuda"))
+        plan.sync()
+        assert torch.equal(b.data, ref_d) and torch.equal(b.par, ref_p), pairs
+        assert torch.equal(b.dbuf[-64:], guard_d) and torch.equal(b.pbuf[-64:], guard_p)
