@@ -966,12 +966,11 @@ def run_xgpu(args):
     from paper_cs_0611109_b200 import raid6c as R
     from paper_cs_0611109_b200 import shard, xgpu
 
-    rank, world, local = _env_rank()
-    local = local % torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group(args.dist_backend, device_id=dev if args.dist_backend == "nccl" else None)
+    rank, world, local, dev, rank_info = init_ranks(args)
+    if world > 1 and args.xgpu != world:
+        print(f"error: --xgpu {args.xgpu} with {world} ranks (one rank per holder: --xgpu G --gpus G)",
+              file=sys.stderr)
+        sys.exit(2)
     c = CONFIGS[args.config]
     p, N = args.prime or c["p"], args.data_strips or c["N"]
     nbytes = args.strip_bytes or c["nbytes"]
@@ -1028,7 +1027,10 @@ def run_xgpu(args):
     for t in range(args.warmup):
         step(t)
     stream.synchronize()
+    snap = None
     if world > 1:
+        if args.verify:
+            snap = xgpu_held_digests(R, torch, X, stream, dev, N, nbytes, pb, S)
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -1041,12 +1043,16 @@ def run_xgpu(args):
     clk = clocks.stop()
     ms = [[ev[t][i].elapsed_time(ev[t][i + 1]) for i in range(4)] for t in range(args.warmup, total)]
     mean = [statistics.mean(m[i] for m in ms) for i in range(4)]
+    per_rank_ms = [round(x, 4) for x in shard.gather_over_ranks(sum(mean), dev)]
     mean = [shard.max_over_ranks(v, dev) for v in mean]
     step_ms = sum(mean)
     # verification (emulation): the layout's P, Q equal the single-GPU encode's, and the recovered
     # strips equal the stripes before the step (recovery in place of intact strips)
-    verified = None
-    if world == 1:
+    verified, base_line = None, None
+    if world > 1 and args.verify:
+        verified, gdig = xgpu_verify_distributed(args, R, torch, X, phase, pair_dev, pairs, snap, stream, dev,
+                                                 N, nbytes, pb, S)
+    elif world == 1:
         ref = par.clone()
         plan.encode_strided(int(data.data_ptr()), X.ss, N * X.ss, int(par.data_ptr()), int(par.data_ptr()) + X.ps,
                             2 * X.ps, S)
@@ -1066,6 +1072,20 @@ def run_xgpu(args):
         R.count_mismatch(par, ref, par.numel(), cnt, stream)
         stream.synchronize()
         verified = {"mismatched_bytes_vs_single_gpu_path": int(cnt.item())}
+        dg = gpu_strip_digests(R, torch, data, par, S, N, X.ss, X.ps, nbytes, pb, stream, dev)
+        gdig = {s_: dg[s_] for s_ in range(S)}
+        verified["ok"] = verified["mismatched_bytes_vs_single_gpu_path"] == 0
+    if verified is not None:
+        # every strip's digest in global stripe order (equal to the single-GPU bench line's for the
+        # same stripes), and the oracle at full size on a sample of stripes: encode + their pair
+        verified["digest_all"] = digest_all(gdig)
+        if rank == 0 and args.cpu_baseline:
+            ver, base_line = oracle_digest_check(p, N, nbytes, args.config, c["sparse"], gdig,
+                                                 {s_: pairs[s_] for s_ in range(S)},
+                                                 8 if args.oracle_stripes is None else args.oracle_stripes,
+                                                 args.cpu_threads)
+            verified.update(ver)
+            verified["ok"] = verified["ok"] and ver["oracle_digest_stripes"] == ver["oracle_digest_sampled"]
     # algorithmic bytes per phase (all G ranks): partial = every surviving strip read once + G
     # partial pairs written; combine = G partial pairs read + 2 rebuilt strips written
     enc_part = S * (N * nbytes + 2 * G * pb)
@@ -1094,14 +1114,85 @@ def run_xgpu(args):
             "roofline": {"kernel": names[dom], "bound": "hbm", "achieved": kern[names[dom]]["achieved_GBps"],
                          "peak": peak, "unit": "GB/s", "frac": kern[names[dom]]["frac_of_peak"],
                          "peak_source": peak_src},
-            "kernels": kern, "gpu_launches": launches, "clocks": clk, "verified": verified}
+            "kernels": kern, "gpu_launches": launches, "clocks": clk, "per_rank_ms": per_rank_ms,
+            "ranks": rank_info, "verified": verified}
+    if base_line is not None:
+        line["cpu_baseline"] = base_line
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()
         X.close()
         dist.barrier()
         dist.destroy_process_group()
     plan.close()
+    if verified is not None and not verified.get("ok", True):
+        sys.exit(3)
+
+
+def xgpu_verify_distributed(args, R, torch, X, phase, pair_dev, pairs, snap, stream, dev, N, nbytes, pb, S):
+    """Untimed checks of the one-process-per-GPU cross-GPU layout (NEXT-4), every rank on the
+    strips it holds: (1) the timed steps left every held strip as it was after the warm-up (each
+    recovery rewrote intact lost strips in place); (2) the lost strips of every stripe are POISONED
+    (0xA5) on their holders and one recovery (partial -> peer slots -> combine -> rebuilt strips
+    stored into their holders' arenas) must restore them; (3) P and Q are poisoned on their
+    holders and one encode must rewrite them.  Compared by per-strip digests against the
+    post-warm-up snapshot; the digests are then gathered on rank 0 for the oracle sample.
+    Returns (verified, {stripe: [d_0..d_{N-1}, P, Q] digests}) (the dict on every rank)."""
+    from paper_cs_0611109_b200 import shard
+    k_lo, k_hi = X.blocks[X.rank]
+    lost = {k: [s_ for s_, pr in enumerate(pairs) if k in pr] for k in range(k_lo, k_hi)}
+
+    def poison(ks, which):
+        with torch.cuda.stream(stream):
+            for k in ks:
+                rows = which(k)
+                if rows:
+                    X.held_strip(k)[:, :(nbytes if k < N else pb)].index_fill_(
+                        0, torch.tensor(rows, device=dev), 0xA5)
+        stream.synchronize()
+
+    def mism(now):
+        return sum(a != b for k in now for a, b in zip(now[k], snap[k]))
+
+    bad_rt = mism(xgpu_held_digests(R, torch, X, stream, dev, N, nbytes, pb, S))
+    poison(range(k_lo, k_hi), lambda k: lost[k])
+    n_poison = sum(len(lost[k]) * (nbytes if k < N else pb) for k in lost)
+    X.barrier(stream)
+    with torch.cuda.stream(stream):
+        phase(0, pair_dev)
+        phase(1, pair_dev)
+    stream.synchronize()
+    bad_rec = mism(xgpu_held_digests(R, torch, X, stream, dev, N, nbytes, pb, S))
+    poison([k for k in range(k_lo, k_hi) if k >= N], lambda k: list(range(S)))
+    X.barrier(stream)
+    with torch.cuda.stream(stream):
+        phase(0, None)
+        phase(1, None)
+    stream.synchronize()
+    now = xgpu_held_digests(R, torch, X, stream, dev, N, nbytes, pb, S)
+    bad_enc = mism(now)
+    tot = shard.sum_over_ranks([bad_rt, bad_rec, bad_enc, n_poison], dev)
+    parts = gather_dict({k: now[k] for k in now})
+    gdig = {s_: [parts[k][s_] for k in range(N + 2)] for s_ in range(S)}
+    ver = {"mismatched_strip_digests": tot[0],
+           "poisoned_recovery": {"poisoned_bytes": tot[3], "mismatched_strip_digests": tot[1]},
+           "fresh_encode_mismatched_strip_digests": tot[2], "ok": tot[0] == tot[1] == tot[2] == 0,
+           "checked": "per-strip digests of every held strip vs the post-warm-up snapshot, on every rank"}
+    return ver, gdig
+
+
+def xgpu_held_digests(R, torch, X, stream, dev, N, nbytes, pb, S):
+    """{k: [S digests]} of the strips this rank holds (raid6c_digest on its arena)."""
+    k_lo, k_hi = X.blocks[X.rank]
+    out = {}
+    for k in range(k_lo, k_hi):
+        t = torch.empty(S, dtype=torch.int64, device=dev)
+        R.digest(X.strip_addr(k), 0, X.stride(k), nbytes if k < N else pb, 1, S, t, stream)
+        out[k] = t
+    stream.synchronize()
+    m = (1 << 64) - 1
+    return {k: [v & m for v in t.cpu().tolist()] for k, t in out.items()}
 
 
 def run_sweep(args):

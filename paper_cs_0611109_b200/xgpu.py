@@ -137,6 +137,14 @@ class Emulated:
             self.combine(g, erasures)
 
 
+class _DevBytes:
+    """A device byte range seen by torch through __cuda_array_interface__ (no copy, no ownership)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
 class Distributed:
     """One process per GPU.  Rank r's arena = its strips [k_lo, k_hi) for S stripes, then its G
     slots (one per source rank) of its word range.  Peer arenas are mapped with CUDA IPC."""
@@ -182,6 +190,17 @@ class Distributed:
 
     def stride(self, k):
         return self.ss if k < self.N else self.ps
+
+    def held_strip(self, k):
+        """Zero-copy uint8 tensor [S, stride(k)] over held strip k in this rank's arena (for
+        verification: poisoning and digests; the path itself takes raw addresses)."""
+        k_lo, k_hi = self.blocks[self.rank]
+        if not (k_lo <= k < k_hi):
+            raise ValueError(f"strip {k} is not held by rank {self.rank}")
+        n = self.S * self.stride(k)
+        buf = _DevBytes(self.strips[k], n)
+        t = self.torch.as_tensor(buf, device=self.torch.device("cuda", self.dev))
+        return t.view(self.S, self.stride(k))
 
     def barrier(self, stream):
         """Every rank's previous launches complete before any rank's next launch starts."""

@@ -51,3 +51,26 @@ def test_full_config_digests_invariant_to_sharding(cfg, stripes):
         assert v["oracle_digest_stripes"] == v["oracle_digest_sampled"] == 4
         out[G] = v["digest_all"]
     assert out[1] == out[2] == out[4], out
+
+
+def test_xgpu_distributed_two_ranks_matches_single_gpu():
+    """NEXT-4 over the self-launched multi-rank path: `--xgpu 2 --gpus 2` brings up two ranks (here
+    sharing cuda:0 under gloo), each holding half of every stripe's strips in an IPC arena; the
+    partial kernel stores into the peer's slots and the combine writes rebuilt strips into their
+    holders.  The line must verify on every rank (round trip, poisoned recovery, fresh encode), the
+    oracle sample must match, and the digests of every strip must equal those of the one-GPU
+    emulation and of the single-GPU bench path on the same stripes (Eq. (PQxy) as sums over disks,
+    PAPER.md:971-979; uniqueness, Lemma 23.2)."""
+    common = ["--config", "2", "--stripes", "4", "--steps", "2", "--warmup", "3", "--oracle-stripes", "2"]
+    d, err = _bench("--gpus", "2", "--dist-backend", "gloo", "--xgpu", "2", *common)
+    v = d["verified"]
+    assert d["n_gpus"] == 2 and len(d["per_rank_ms"]) == 2 and d["ranks"]["ranks_up"] == 2
+    assert not d["config"]["emulated"]
+    assert v["ok"] and v["mismatched_strip_digests"] == 0
+    assert v["poisoned_recovery"]["poisoned_bytes"] > 0 and v["poisoned_recovery"]["mismatched_strip_digests"] == 0
+    assert v["fresh_encode_mismatched_strip_digests"] == 0
+    assert v["oracle_digest_stripes"] == v["oracle_digest_sampled"] == 2
+    e, _ = _bench("--gpus", "1", "--xgpu", "2", *common)
+    assert e["config"]["emulated"] and e["verified"]["ok"]
+    s, _ = _bench("--gpus", "1", "--no-e2e", *common)
+    assert v["digest_all"] == e["verified"]["digest_all"] == s["verified"]["digest_all"]
