@@ -86,7 +86,15 @@ struct Geo {
   // not below 20 lanes: 128 threads for p = 73, 97, 113, 137, 193, 241 (12-18 lanes) cost recovery 11-31 %
   static constexpr int THREADS = SMALL8 ? 256 : (C >= 20 ? 128 : ((32 % n == 0) ? 224 : (REC_ ? ZP_REC_THREADS : 256)));
   static constexpr int TB = THREADS * CB;            // TMA row (tile) bytes
-  static constexpr int MTAB = (n + 1) * LAMBDA;      // mask table entries (uint2)
+  // Mask table: MX(a), ML(a) per rotation amount a and lane phase (uint2), or -- when that would
+  // take more than 40 KB of shared memory (p = 233: 53 KB, leaving 2 TMA stages at 2 CTAs/SM) --
+  // ML(a) alone for a = 0..n+1 (uint32), with MX(a) = ~ML(a+1) | M0 derived in the fold
+  // (ML(a+1) = word positions 0..a-1, so its complement plus position 0 is MX(a)).  Not for
+  // recovery, whose rotations are the bottleneck: measured p = 233 encode 0.95 -> 1.02 of the
+  // copy rate with the half table (3 stages), recovery 0.575 -> 0.553 (one more LOP3 per lane).
+  static constexpr bool HALF = (n + 1) * LAMBDA * 8 > 40 * 1024 && !REC_;
+  static constexpr int MTAB = HALF ? (n + 2) * LAMBDA : (n + 1) * LAMBDA;  // entries
+  static constexpr int MTAB_BYTES = MTAB * (HALF ? 4 : 8);
   static_assert(LAMBDA <= 32, "fast path needs a period of at most 32 lanes");
   static_assert(TB % 16 == 0, "TMA rows must be multiples of 16 bytes");
 };
@@ -258,6 +266,23 @@ struct Acc {
   }
 };
 
+// (MX(a), ML(a)) of lane phase phi from row a of the mask table (see Geo::HALF).
+template <class G>
+__device__ __forceinline__ uint2 mask_pair(const uint2* __restrict__ mrow, int phi) {
+  if constexpr (G::HALF) {
+    const uint32_t* r = reinterpret_cast<const uint32_t*>(mrow);
+    return make_uint2(~r[G::LAMBDA + phi] | m0_mask<G::n>(phi), r[phi]);
+  } else {
+    return mrow[phi];
+  }
+}
+// Row a of the mask table.
+template <class G>
+__device__ __forceinline__ const uint2* mask_row(const uint2* __restrict__ mtab, int a) {
+  if constexpr (G::HALF) return reinterpret_cast<const uint2*>(reinterpret_cast<const uint32_t*>(mtab) + a * G::LAMBDA);
+  else return mtab + a * G::LAMBDA;
+}
+
 // acc += x^a * S for a in [1, n], lane shift Q = a>>5 (left) and QP = (p-a)>>5 (right).
 template <class G, int Q, int QP>
 __device__ __forceinline__ void rot_body(const uint32_t (&S)[G::C], uint32_t r, uint32_t rp,
@@ -265,7 +290,7 @@ __device__ __forceinline__ void rot_body(const uint32_t (&S)[G::C], uint32_t r, 
   constexpr int C = G::C;
 #pragma unroll
   for (int l = 0; l < C; l++) {
-    const uint2 m = mrow[l % G::LAMBDA];
+    const uint2 m = mask_pair<G>(mrow, l % G::LAMBDA);
     const uint32_t xh = (l - Q >= 0) ? S[l - Q >= 0 ? l - Q : 0] : 0u;
     const uint32_t xl = (l - Q - 1 >= 0) ? S[l - Q - 1 >= 0 ? l - Q - 1 : 0] : 0u;
     const uint32_t X = __funnelshift_l(xl, xh, r);
@@ -309,11 +334,11 @@ template <class G>
 __device__ __forceinline__ void rot_acc_nz(const uint32_t (&S)[G::C], int a, const uint2* __restrict__ mtab,
                                            Acc<G>& acc) {
   if constexpr (G::QMAX == 0 && G::P <= 32) {  // words below 32 bits: no whole-lane shift to dispatch
-    rot_body<G, 0, 0>(S, static_cast<uint32_t>(a), static_cast<uint32_t>(G::P - a), mtab + a * G::LAMBDA, acc);
+    rot_body<G, 0, 0>(S, static_cast<uint32_t>(a), static_cast<uint32_t>(G::P - a), mask_row<G>(mtab, a), acc);
   } else {
     const int q = a >> 5, qp = (G::P - a) >> 5;
     const uint32_t r = static_cast<uint32_t>(a & 31), rp = static_cast<uint32_t>((G::P - a) & 31);
-    rot_dispatch<G, 0>(q * (G::QMAX + 1) + qp, S, r, rp, mtab + a * G::LAMBDA, acc);
+    rot_dispatch<G, 0>(q * (G::QMAX + 1) + qp, S, r, rp, mask_row<G>(mtab, a), acc);
   }
 }
 
@@ -930,7 +955,8 @@ __device__ __forceinline__ void build_mtab(uint2* mtab) {
       if (pos + 2 <= am) ml |= 1u << b;
       if (++pos == G::n) pos = 0;
     }
-    mtab[e] = make_uint2(mx, ml);
+    if constexpr (G::HALF) reinterpret_cast<uint32_t*>(mtab)[e] = ml;
+    else mtab[e] = make_uint2(mx, ml);
   }
 }
 
@@ -953,9 +979,9 @@ struct Layout {
   using G = GeoM<P, MODE>;
   static constexpr int NOUT = num_outputs<MODE>();
   static constexpr int SMEM_TARGET = min_blocks<P, MODE>() == 3 ? 72 * 1024 : 112 * 1024;
-  static constexpr int STAGES_RAW = (SMEM_TARGET - NOUT * G::TB - G::MTAB * 8 - 256) / G::TB;
+  static constexpr int STAGES_RAW = (SMEM_TARGET - NOUT * G::TB - G::MTAB_BYTES - 256) / G::TB;
   static constexpr size_t smem_for(int st) {
-    return (size_t)(st + NOUT) * G::TB + (size_t)G::MTAB * 8 + 2 * st * 8;
+    return (size_t)(st + NOUT) * G::TB + (size_t)G::MTAB_BYTES + 2 * st * 8;
   }
   static constexpr bool fits(int st) { return (smem_for(st) + 1024) * min_blocks<P, MODE>() <= 228 * 1024; }
   // at least 3 stages; 2 only where 3 would cost a CTA per SM (large mask tables: p = 233
@@ -1033,7 +1059,7 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
   uint8_t* stages = smem;
   uint8_t* outb = smem + (size_t)ST * TB;
   uint2* mtab = reinterpret_cast<uint2*>(outb + (size_t)NOUT * TB);
-  uint64_t* full = reinterpret_cast<uint64_t*>(mtab + G::MTAB);
+  uint64_t* full = reinterpret_cast<uint64_t*>(outb + (size_t)NOUT * TB + G::MTAB_BYTES);
   uint64_t* empty = full + ST;
 
   const int tid = threadIdx.x;
