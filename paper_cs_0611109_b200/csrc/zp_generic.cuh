@@ -16,12 +16,19 @@
 //     Sec. 4.6), the DD inverse by the same doubling chain; outputs are
 //     packed at compile-time offsets and written with aligned 32-bit stores (byte stores only
 //     at the group's edges).
-// No TMA and no shared memory.
+// Encode and recovery of the basic code (N <= p) run the TMA-staged variant
+// (zp_generic_tma_kernel: the same group arithmetic fed from a shared-memory ring, outputs
+// bulk-stored); the other modes, the extended code and unaligned strips use zp_generic_kernel
+// (direct global loads, no shared memory).
 #include <algorithm>
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <type_traits>
 #include <cuda_runtime.h>
 
+#include "tma_ring.cuh"
 #include "zp_args.h"
 
 namespace zp {
@@ -354,6 +361,16 @@ __device__ __forceinline__ void finish_word(const ZpArgs& a, const Desc& d, int 
   }
 }
 
+// Output strips of a class (update: P, Q -- d_k was stored with its row; scrub: none).
+__device__ __forceinline__ void out_strips(const ZpArgs& a, const Desc& d, int (&kout)[2], int& nout) {
+  if (d.cls == 0) { kout[0] = a.N; kout[1] = a.N + 1; }
+  else if (d.cls == 1) { kout[0] = d.x; kout[1] = a.N + 1; }
+  else if (d.cls == 2) { kout[0] = d.x; kout[1] = a.N; }
+  else if (d.cls == 3) { kout[0] = d.x; kout[1] = d.y; }
+  else if (d.cls == 4) { nout = 0; }
+  else { kout[0] = a.N; kout[1] = a.N + 1; }
+}
+
 template <int P, int WI>
 struct GroupWords {  // compile-time loop over the group's words
   template <class F>
@@ -365,94 +382,241 @@ struct GroupWords {  // compile-time loop over the group's words
   }
 };
 
+// One group (g words) of stripe s through the direct path: aligned 32-bit global loads of each
+// row, fold, class epilogue, aligned stores (byte stores at the group's edges).
+template <int P>
+__device__ __forceinline__ void group_direct(const ZpArgs& a, int mode, int s, uint64_t grp, uint64_t W) {
+  using GG = GP<P>;
+  constexpr int NL = GG::NL, g = GG::g, GB = GG::GB, W4 = GG::W4;
+  const uint64_t byte0 = grp * static_cast<uint64_t>(GB);
+  const Desc d = desc_of(a, s, mode, P);
+  const bool ext = a.N > P;
+  // rows: partial = this rank's surviving strips [k_lo, k_hi); combine = nsrc partial slots
+  int R = mode == KMODE_SCRUB ? a.N + 2 : (mode == KMODE_UPDATE ? a.upd_rows : a.N);
+  if (mode == KMODE_PARTIAL)
+    R = a.k_hi - a.k_lo - (d.x >= a.k_lo && d.x < a.k_hi) - (d.y >= a.k_lo && d.y < a.k_hi);
+  if (mode == KMODE_COMBINE) R = a.nsrc;
+  Word<NL> Pa[g], acc[g];
+#pragma unroll
+  for (int wi = 0; wi < g; wi++) {
+    wzero(Pa[wi]);
+    wzero(acc[wi]);
+  }
+  uint32_t buf[W4 + 1];
+  for (int r = 0; r < R; r++) {
+    if (mode == KMODE_COMBINE) {  // partial slots hold reduced words of bytes [range_lo, ...)
+      const uint64_t so = static_cast<uint64_t>(s) * a.part_stride;
+      const uint64_t off = byte0 - a.range_lo, ll = a.pbytes - a.range_lo;
+      load_group<W4>(a.src_p[r] + so, ll, off, buf);
+      GroupWords<P, 0>::run([&](auto wc) {
+        Word<NL> L;
+        group_word<P, decltype(wc)::value>(buf, L);
+        wxor(Pa[decltype(wc)::value], L);
+      });
+      load_group<W4>(a.src_q[r] + so, ll, off, buf);
+      GroupWords<P, 0>::run([&](auto wc) {
+        Word<NL> L;
+        group_word<P, decltype(wc)::value>(buf, L);
+        wxor(acc[decltype(wc)::value], L);
+      });
+      continue;
+    }
+    int k;
+    if (mode == KMODE_SCRUB) k = r;
+    else if (mode == KMODE_UPDATE) k = r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
+    else {
+      k = mode == KMODE_PARTIAL ? a.k_lo + r : r;
+      const int lo = mode == KMODE_PARTIAL ? a.k_lo : 0;
+      if (d.x >= lo && k >= d.x) k++;
+      if (d.y >= lo && k >= d.y) k++;
+    }
+    load_group<W4>(rptr(a, k, s), rlen(a, k), byte0, buf);
+    if (k == K_NEW) {
+      // update: the new bytes go straight to the rewritten strip (this group's bytes of it were
+      // read as row 0; bytes of neighbouring groups that the aligned loads touch are masked off)
+      const uint64_t left = a.bytes > byte0 ? a.bytes - byte0 : 0;
+      store_group<W4>(const_cast<uint8_t*>(rptr(a, d.x, s)) + byte0,
+                      static_cast<int>(left < static_cast<uint64_t>(GB) ? left : GB), buf);
+      k = d.x;
+    }
+    int amt = 0;
+    if (!(ext && k < a.N)) {
+      amt = ((k < a.N ? k : P) - d.base) % P;
+      if (amt < 0) amt += P;
+    }
+    GroupWords<P, 0>::run([&](auto wc) {
+      constexpr int WI = decltype(wc)::value;
+      Word<NL> L;
+      group_word<P, WI>(buf, L);
+      if (k <= a.N) wxor(Pa[WI], L);
+      if (k != a.N) {
+        if (ext && k < a.N) add_coeff(acc[WI], L, k, P);
+        else rot_acc(acc[WI], L, amt, P);
+      }
+    });
+  }
+  int kout[2] = {0, 0};
+  int nout = 2;
+  out_strips(a, d, kout, nout);
+  uint32_t ob[2][W4 + 1];
+#pragma unroll
+  for (int q = 0; q < 2; q++)
+#pragma unroll
+    for (int i = 0; i <= W4; i++) ob[q][i] = 0;
+  uint32_t bad = 0;
+  GroupWords<P, 0>::run([&](auto wc) {
+    constexpr int WI = decltype(wc)::value;
+    Word<NL> o[2];
+    finish_word<NL>(a, d, P, mode, ext, Pa[WI], acc[WI], o, grp * g + WI < W, bad);
+#pragma unroll
+    for (int q = 0; q < 2; q++)
+      if (q < nout) group_put<P, WI>(ob[q], o[q]);
+  });
+  if (mode == KMODE_SCRUB) {
+    if (bad) atomicAdd(a.counts + s, bad);
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < 2; q++) {
+    if (q >= nout) break;
+    uint8_t* gq;  // address of byte byte0 of output q
+    uint64_t left;
+    if (mode == KMODE_PARTIAL) {  // slot of the owner of this word range
+      const int own = static_cast<int>(byte0 / a.range_bytes);
+      gq = (q == 0 ? a.part_p[own] : a.part_q[own]) + static_cast<uint64_t>(s) * a.part_stride +
+           (byte0 - static_cast<uint64_t>(own) * a.range_bytes);
+      left = a.pbytes > byte0 ? a.pbytes - byte0 : 0;
+    } else {
+      gq = const_cast<uint8_t*>(rptr(a, kout[q], s)) + byte0;
+      const uint64_t len = rlen(a, kout[q]);
+      left = len > byte0 ? len - byte0 : 0;
+    }
+    const int nb = static_cast<int>(left < static_cast<uint64_t>(GB) ? left : GB);
+    store_group<W4>(gq, nb, ob[q]);
+  }
+}
+
 template <int P>
 __global__ void __launch_bounds__(128, GP<P>::MINB) zp_generic_kernel(const __grid_constant__ ZpArgs a, int mode) {
   using GG = GP<P>;
-  constexpr int n = GG::n, NL = GG::NL, g = GG::g, GB = GG::GB, W4 = GG::W4;
-  const uint64_t W = (8 * a.bytes + n - 1) / n;
+  const uint64_t W = (8 * a.bytes + GG::n - 1) / GG::n;
   uint64_t g0, g1;
-  group_span(a, mode, n, g, GB, g0, g1);
+  group_span(a, mode, GG::n, GG::g, GG::GB, g0, g1);
   const uint64_t groups = g1 - g0;
   const uint64_t total = groups * static_cast<uint64_t>(a.num_stripes);
   for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < total;
        u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int s = static_cast<int>(u / groups);
-    const uint64_t grp = g0 + (u - static_cast<uint64_t>(s) * groups);
-    const uint64_t byte0 = grp * static_cast<uint64_t>(GB);
-    const Desc d = desc_of(a, s, mode, P);
-    const bool ext = a.N > P;
-    // rows: partial = this rank's surviving strips [k_lo, k_hi); combine = nsrc partial slots
-    int R = mode == KMODE_SCRUB ? a.N + 2 : (mode == KMODE_UPDATE ? a.upd_rows : a.N);
-    if (mode == KMODE_PARTIAL)
-      R = a.k_hi - a.k_lo - (d.x >= a.k_lo && d.x < a.k_hi) - (d.y >= a.k_lo && d.y < a.k_hi);
-    if (mode == KMODE_COMBINE) R = a.nsrc;
+    group_direct<P>(a, mode, s, g0 + (u - static_cast<uint64_t>(s) * groups), W);
+  }
+}
+
+// ---------------------------------------------------------------- TMA-staged encode / recovery
+// The same group arithmetic fed from a TMA ring (the fast kernel's producer/consumer scheme,
+// tma_ring.cuh): a tile = 128 consecutive groups of one stripe (TB = 128 * GB bytes, a multiple
+// of 16); one producer lane streams the tile rows of the N surviving strips HBM -> SMEM with
+// cp.async.bulk; consumer thread t reads group t of each row from SMEM (aligned 32-bit loads,
+// one funnel shift), folds it, runs the class epilogue, packs the outputs into two SMEM output
+// tiles, and thread 0 bulk-stores them.  The groups past the last whole tile (and every group
+// when a strip is not 16-byte aligned) go through group_direct.  Basic code (N <= p), encode and
+// recovery only; the other modes and the extended code keep zp_generic_kernel.
+template <int P>
+struct GT {
+  using GG = GP<P>;
+  static constexpr int NT = 128;                  // consumer threads = groups per tile
+  static constexpr int TB = NT * GG::GB;          // tile bytes
+  static constexpr int MINB = GG::NL * GG::g <= 20 ? 3 : 2;  // CTAs per SM (160 threads each)
+  static constexpr int BUDGET = (227 * 1024) / MINB - 1024;
+  static constexpr int ST_RAW = (BUDGET - 2 * TB - 128) / TB;
+  static constexpr int ST = ST_RAW < 2 ? 2 : (ST_RAW > 8 ? 8 : ST_RAW);
+  static constexpr size_t SMEM = static_cast<size_t>(ST + 2) * TB + 2 * ST * 8 + 16;
+  static_assert(TB % 16 == 0, "TMA rows are multiples of 16 bytes");
+};
+
+template <int P, int MODE>
+__global__ void __launch_bounds__(GT<P>::NT + 32, GT<P>::MINB) zp_generic_tma_kernel(const __grid_constant__ ZpArgs a) {
+  using GG = GP<P>;
+  using T = GT<P>;
+  constexpr int NL = GG::NL, g = GG::g, GB = GG::GB, W4 = GG::W4, NT = T::NT, TB = T::TB, ST = T::ST;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* stages = smem;
+  uint8_t* outb = smem + static_cast<size_t>(ST) * TB;
+  // (one 16-byte pad after the output tiles: the last group's aligned loads may read a word past
+  // its stage, never past the allocation)
+  uint64_t* full = reinterpret_cast<uint64_t*>(outb + 2 * static_cast<size_t>(TB) + 16);
+  uint64_t* empty = full + ST;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < ST; i++) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], NT / 32);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const uint64_t tiles = a.body_tiles;
+  const uint64_t items = tiles * static_cast<uint64_t>(a.num_stripes);
+  if (warp == NT / 32) {  // producer: one lane issues every row of every item
+    if (lane == 0) {
+      uint32_t stage = 0, ph = 0;
+      for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const int s = static_cast<int>(it / tiles);
+        const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
+        const Desc d = desc_of(a, s, MODE, P);
+        for (int r = 0; r < a.N; r++) {
+          int k = r;
+          if (k >= d.x) k++;
+          if (k >= d.y) k++;
+          mbar_wait(&empty[stage], ph ^ 1u);
+          mbar_expect_tx(&full[stage], TB);
+          tma_load_row(stages + static_cast<size_t>(stage) * TB, rptr(a, k, s) + t * TB, TB, &full[stage]);
+          if (++stage == ST) { stage = 0; ph ^= 1u; }
+        }
+      }
+    }
+    return;
+  }
+  const uint32_t full_sa = smem_u32(full), empty_sa = smem_u32(empty);
+  uint32_t stage = 0, ph = 0;
+  const uint32_t mis = static_cast<uint32_t>(tid * GB) & 3u;
+  const uint32_t* my = reinterpret_cast<const uint32_t*>(stages + (tid * GB - mis));
+  for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int s = static_cast<int>(it / tiles);
+    const uint64_t t = it - static_cast<uint64_t>(s) * tiles;
+    const Desc d = desc_of(a, s, MODE, P);
     Word<NL> Pa[g], acc[g];
 #pragma unroll
     for (int wi = 0; wi < g; wi++) {
       wzero(Pa[wi]);
       wzero(acc[wi]);
     }
-    uint32_t buf[W4 + 1];
-    for (int r = 0; r < R; r++) {
-      if (mode == KMODE_COMBINE) {  // partial slots hold reduced words of bytes [range_lo, ...)
-        const uint64_t so = static_cast<uint64_t>(s) * a.part_stride;
-        const uint64_t off = byte0 - a.range_lo, ll = a.pbytes - a.range_lo;
-        load_group<W4>(a.src_p[r] + so, ll, off, buf);
-        GroupWords<P, 0>::run([&](auto wc) {
-          Word<NL> L;
-          group_word<P, decltype(wc)::value>(buf, L);
-          wxor(Pa[decltype(wc)::value], L);
-        });
-        load_group<W4>(a.src_q[r] + so, ll, off, buf);
-        GroupWords<P, 0>::run([&](auto wc) {
-          Word<NL> L;
-          group_word<P, decltype(wc)::value>(buf, L);
-          wxor(acc[decltype(wc)::value], L);
-        });
-        continue;
-      }
-      int k;
-      if (mode == KMODE_SCRUB) k = r;
-      else if (mode == KMODE_UPDATE) k = r == 0 ? d.x : (r == 1 ? K_NEW : a.N + r - 2);
-      else {
-        k = mode == KMODE_PARTIAL ? a.k_lo + r : r;
-        const int lo = mode == KMODE_PARTIAL ? a.k_lo : 0;
-        if (d.x >= lo && k >= d.x) k++;
-        if (d.y >= lo && k >= d.y) k++;
-      }
-      load_group<W4>(rptr(a, k, s), rlen(a, k), byte0, buf);
-      if (k == K_NEW) {
-        // update: the new bytes go straight to the rewritten strip (this group's bytes of it were
-        // read as row 0; bytes of neighbouring groups that the aligned loads touch are masked off)
-        const uint64_t left = a.bytes > byte0 ? a.bytes - byte0 : 0;
-        store_group<W4>(const_cast<uint8_t*>(rptr(a, d.x, s)) + byte0,
-                        static_cast<int>(left < static_cast<uint64_t>(GB) ? left : GB), buf);
-        k = d.x;
-      }
-      int amt = 0;
-      if (!(ext && k < a.N)) {
-        amt = ((k < a.N ? k : P) - d.base) % P;
-        if (amt < 0) amt += P;
-      }
+    for (int r = 0; r < a.N; r++) {
+      int k = r;
+      if (k >= d.x) k++;
+      if (k >= d.y) k++;
+      mbar_wait_sa(full_sa + 8u * stage, ph);
+      const uint32_t* q = my + static_cast<size_t>(stage) * (TB / 4);
+      uint32_t raw[W4 + 1], buf[W4 + 1];
+#pragma unroll
+      for (int i = 0; i <= W4; i++) raw[i] = q[i];
+#pragma unroll
+      for (int i = 0; i < W4; i++) buf[i] = __funnelshift_r(raw[i], raw[i + 1], 8 * mis);
+      buf[W4] = 0u;
+      int amt = ((k < a.N ? k : P) - d.base) % P;
+      if (amt < 0) amt += P;
       GroupWords<P, 0>::run([&](auto wc) {
         constexpr int WI = decltype(wc)::value;
         Word<NL> L;
         group_word<P, WI>(buf, L);
         if (k <= a.N) wxor(Pa[WI], L);
-        if (k != a.N) {
-          if (ext && k < a.N) add_coeff(acc[WI], L, k, P);
-          else rot_acc(acc[WI], L, amt, P);
-        }
+        if (k != a.N) rot_acc(acc[WI], L, amt, P);
       });
+      consumer_release(empty_sa + 8u * stage, lane);
+      if (++stage == ST) { stage = 0; ph ^= 1u; }
     }
     int kout[2] = {0, 0};
     int nout = 2;
-    if (d.cls == 0) { kout[0] = a.N; kout[1] = a.N + 1; }
-    else if (d.cls == 1) { kout[0] = d.x; kout[1] = a.N + 1; }
-    else if (d.cls == 2) { kout[0] = d.x; kout[1] = a.N; }
-    else if (d.cls == 3) { kout[0] = d.x; kout[1] = d.y; }
-    else if (d.cls == 4) { nout = 0; }
-    else { kout[0] = a.N; kout[1] = a.N + 1; }  // update: P, Q (d_k was stored with its row)
+    out_strips(a, d, kout, nout);
     uint32_t ob[2][W4 + 1];
 #pragma unroll
     for (int q = 0; q < 2; q++)
@@ -462,39 +626,94 @@ __global__ void __launch_bounds__(128, GP<P>::MINB) zp_generic_kernel(const __gr
     GroupWords<P, 0>::run([&](auto wc) {
       constexpr int WI = decltype(wc)::value;
       Word<NL> o[2];
-      finish_word<NL>(a, d, P, mode, ext, Pa[WI], acc[WI], o, grp * g + WI < W, bad);
-#pragma unroll
-      for (int q = 0; q < 2; q++)
-        if (q < nout) group_put<P, WI>(ob[q], o[q]);
+      finish_word<NL>(a, d, P, MODE, false, Pa[WI], acc[WI], o, true, bad);
+      group_put<P, WI>(ob[0], o[0]);
+      group_put<P, WI>(ob[1], o[1]);
     });
-    if (mode == KMODE_SCRUB) {
-      if (bad) atomicAdd(a.counts + s, bad);
-      continue;
-    }
-#pragma unroll
-    for (int q = 0; q < 2; q++) {
-      if (q >= nout) break;
-      uint8_t* gq;  // address of byte byte0 of output q
-      uint64_t left;
-      if (mode == KMODE_PARTIAL) {  // slot of the owner of this word range
-        const int own = static_cast<int>(byte0 / a.range_bytes);
-        gq = (q == 0 ? a.part_p[own] : a.part_q[own]) + static_cast<uint64_t>(s) * a.part_stride +
-             (byte0 - static_cast<uint64_t>(own) * a.range_bytes);
-        left = a.pbytes > byte0 ? a.pbytes - byte0 : 0;
-      } else {
-        gq = const_cast<uint8_t*>(rptr(a, kout[q], s)) + byte0;
-        const uint64_t len = rlen(a, kout[q]);
-        left = len > byte0 ? len - byte0 : 0;
-      }
-      const int nb = static_cast<int>(left < static_cast<uint64_t>(GB) ? left : GB);
-      store_group<W4>(gq, nb, ob[q]);
+    if (tid == 0) bulk_wait_read0();  // the previous item's bulk stores have read the tiles
+    named_bar_sync(1, NT);
+    store_group<W4>(outb + tid * GB, GB, ob[0]);
+    store_group<W4>(outb + TB + tid * GB, GB, ob[1]);
+    fence_proxy_async_smem();
+    named_bar_sync(1, NT);
+    if (tid == 0) {
+      tma_store_row(const_cast<uint8_t*>(rptr(a, kout[0], s)) + t * TB, outb, TB);
+      tma_store_row(const_cast<uint8_t*>(rptr(a, kout[1], s)) + t * TB, outb + TB, TB);
+      bulk_commit();
     }
   }
+  // groups past the body tiles: direct path, one group per consumer thread
+  const uint64_t W = (8 * a.bytes + GG::n - 1) / GG::n;
+  const uint64_t groups = (W + g - 1) / g;
+  const uint64_t gbody = tiles * NT;
+  const uint64_t tail = groups > gbody ? groups - gbody : 0;
+  const uint64_t total = tail * static_cast<uint64_t>(a.num_stripes);
+  for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * NT + tid; u < total; u += static_cast<uint64_t>(gridDim.x) * NT) {
+    const int s = static_cast<int>(u / tail);
+    group_direct<P>(a, MODE, s, gbody + (u - static_cast<uint64_t>(s) * tail), W);
+  }
+  if (tid == 0) bulk_wait0();
+}
+
+// CTAs per SM of a TMA kernel on the current device (dynamic shared memory attribute set once
+// per device and kernel).
+inline cudaError_t tma_occupancy(const void* fn, size_t smem, int threads, int* occ) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(dev, fn);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *occ = it->second;
+    return cudaSuccess;
+  }
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int o = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (o < 1) o = 1;
+  cache[key] = o;
+  *occ = o;
+  return cudaSuccess;
 }
 
 template <int P>
 cudaError_t launch_p(const ZpArgs& a, int mode, cudaStream_t st, int num_sms) {
   using GG = GP<P>;
+  // (3, 7, 31, 73 reach this kernel only with the extended code)
+  if constexpr (!(P == 3 || P == 7 || P == 31 || P == 73)) {
+    using T = GT<P>;
+    if ((mode == KMODE_ENCODE || mode == KMODE_RECOVER) && a.N <= P && a.bytes >= static_cast<uint64_t>(T::TB)) {
+      bool aligned = true;
+      for (int k = 0; k < a.N + 2; k++) aligned &= (reinterpret_cast<uintptr_t>(a.base[k]) & 15u) == 0;
+      if (a.num_stripes > 1) aligned &= (a.data_stride % 16 == 0) && (a.parity_stride % 16 == 0);
+      if (aligned) {
+        ZpArgs b = a;
+        b.body_tiles = a.bytes / T::TB;
+        const void* fn = mode == KMODE_ENCODE ? reinterpret_cast<const void*>(&zp_generic_tma_kernel<P, KMODE_ENCODE>)
+                                              : reinterpret_cast<const void*>(&zp_generic_tma_kernel<P, KMODE_RECOVER>);
+        int occ = 1;
+        cudaError_t e = tma_occupancy(fn, T::SMEM, T::NT + 32, &occ);
+        if (e != cudaSuccess) return e;
+        const uint64_t W = (8 * a.bytes + GG::n - 1) / GG::n;
+        const uint64_t groups = (W + GG::g - 1) / GG::g;
+        const uint64_t tail = groups - b.body_tiles * T::NT;
+        const uint64_t items = b.body_tiles * static_cast<uint64_t>(a.num_stripes);
+        const uint64_t tail_ctas = (tail * static_cast<uint64_t>(a.num_stripes) + T::NT - 1) / T::NT;
+        const uint64_t cap = static_cast<uint64_t>(num_sms) * occ;
+        uint64_t grid = std::min<uint64_t>(cap, std::max<uint64_t>(items, tail_ctas));
+        if (grid == 0) grid = 1;
+        void* args[] = {&b};
+        e = cudaLaunchKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(T::NT + 32), args, T::SMEM, st);
+        if (e != cudaSuccess) return e;
+        return cudaGetLastError();
+      }
+    }
+  }
   uint64_t g0 = 0, g1 = ((8 * a.bytes + GG::n - 1) / GG::n + GG::g - 1) / GG::g;
   if (mode == KMODE_COMBINE) {
     g0 = a.range_lo / GG::GB;
