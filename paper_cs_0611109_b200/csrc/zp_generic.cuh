@@ -99,6 +99,58 @@ __device__ __forceinline__ void rot_acc(Word<NL>& acc, const Word<NL>& src, int 
   for (int i = 0; i < NL; i++) acc.v[i] ^= (l.v[i] | r.v[i]) & low_mask(p, i);
 }
 
+// The same rotation for a compile-time p with the whole-limb parts of both shifts dispatched to
+// compile-time limb offsets: acc ^= (src << a) ^ (src >> (p - a)) limb by limb, one funnel shift
+// per limb and shift instead of a funnel stage plus a log2(NL)-step select barrel (the two parts
+// occupy disjoint bits [a, p) and [0, a) of the slot).  Q1 = a >> 5; Q2 = (p - a) >> 5 takes one
+// of two values for a given Q1.
+template <int P, int Q1, int Q2>
+__device__ __forceinline__ void rot_static(Word<(P + 31) / 32>& acc, const Word<(P + 31) / 32>& src, uint32_t r1,
+                                           uint32_t r2) {
+  constexpr int NL = (P + 31) / 32;
+#pragma unroll
+  for (int i = 0; i < NL; i++) {
+    const uint32_t lh = (i - Q1 >= 0 && i - Q1 < NL) ? src.v[(i - Q1 >= 0 && i - Q1 < NL) ? i - Q1 : 0] : 0u;
+    const uint32_t ll = (i - Q1 - 1 >= 0 && i - Q1 - 1 < NL) ? src.v[(i - Q1 - 1 >= 0 && i - Q1 - 1 < NL) ? i - Q1 - 1 : 0] : 0u;
+    const uint32_t rl = (i + Q2 < NL) ? src.v[(i + Q2 < NL) ? i + Q2 : 0] : 0u;
+    const uint32_t rh = (i + Q2 + 1 < NL) ? src.v[(i + Q2 + 1 < NL) ? i + Q2 + 1 : 0] : 0u;
+    const uint32_t v = __funnelshift_l(ll, lh, r1) ^ __funnelshift_r(rl, rh, r2);
+    acc.v[i] ^= (32 * (i + 1) <= P) ? v : (v & low_mask(P, i));
+  }
+}
+template <int P, int Q1>
+__device__ __forceinline__ void rot_q1(Word<(P + 31) / 32>& acc, const Word<(P + 31) / 32>& src, uint32_t r1, int q2,
+                                       uint32_t r2) {
+  constexpr int QB = (P - 32 * Q1) >> 5;
+  constexpr int QA = (P - 32 * Q1 - 31) >= 0 ? (P - 32 * Q1 - 31) >> 5 : 0;
+  if constexpr (QA == QB) {
+    rot_static<P, Q1, QB>(acc, src, r1, r2);
+  } else {
+    if (q2 == QB) rot_static<P, Q1, QB>(acc, src, r1, r2);
+    else rot_static<P, Q1, QA>(acc, src, r1, r2);
+  }
+}
+template <int P, int Q1 = 0>
+__device__ __forceinline__ void rot_dispatch_q(int q1, Word<(P + 31) / 32>& acc, const Word<(P + 31) / 32>& src,
+                                               uint32_t r1, int q2, uint32_t r2) {
+  if constexpr (32 * Q1 < P) {
+    if (q1 == Q1) {
+      rot_q1<P, Q1>(acc, src, r1, q2, r2);
+      return;
+    }
+    rot_dispatch_q<P, Q1 + 1>(q1, acc, src, r1, q2, r2);
+  }
+}
+template <int P>
+__device__ __forceinline__ void rot_acc_t(Word<(P + 31) / 32>& acc, const Word<(P + 31) / 32>& src, int a) {
+  if (a == 0) {
+    wxor(acc, src);
+    return;
+  }
+  const int b = P - a;
+  rot_dispatch_q<P>(a >> 5, acc, src, static_cast<uint32_t>(a & 31), b >> 5, static_cast<uint32_t>(b & 31));
+}
+
 // pi: if slot bit p-1 is set, flip bits 0..n-1 and clear bit p-1.
 template <int NL>
 __device__ __forceinline__ void reduce(Word<NL>& w, int p) {
@@ -280,9 +332,10 @@ __device__ __forceinline__ void store_group(uint8_t* dst, int nb, const uint32_t
 }
 
 // Class epilogue of one word: o[0..nout) from the folded Pa / acc.
-template <int NL>
-__device__ __forceinline__ void finish_word(const ZpArgs& a, const Desc& d, int p, int mode, bool ext, Word<NL>& Pa,
+template <int P, int NL = (P + 31) / 32>
+__device__ __forceinline__ void finish_word(const ZpArgs& a, const Desc& d, int mode, bool ext, Word<NL>& Pa,
                                             Word<NL>& acc, Word<NL> (&o)[2], bool valid, uint32_t& bad) {
+  constexpr int p = P;
   const ExtProg* pr = ext ? a.prog + pair_index(d.x, d.y, a.N) : nullptr;
   if (mode == KMODE_PARTIAL) {  // unsolved partial syndromes (NEXT-4)
     o[0] = Pa;
@@ -312,7 +365,7 @@ __device__ __forceinline__ void finish_word(const ZpArgs& a, const Desc& d, int 
     o[1] = acc;
   } else if (d.cls == 1) {
     o[0] = Pa;
-    rot_acc(acc, Pa, d.x, p);
+    rot_acc_t<P>(acc, Pa, d.x);
     reduce(acc, p);
     o[1] = acc;
   } else if (d.cls == 2) {
@@ -332,13 +385,13 @@ __device__ __forceinline__ void finish_word(const ZpArgs& a, const Desc& d, int 
 #pragma unroll 1
     for (int bit = top - 1; bit >= 0; bit--) {
       Word<NL> nx = S;
-      rot_acc(nx, S, (bz * m) % p, p);
+      rot_acc_t<P>(nx, S, (bz * m) % p);
       reduce(nx, p);
       S = nx;
       m *= 2;
       if ((M >> bit) & 1) {
         nx = S;
-        rot_acc(nx, t, (bz * m) % p, p);
+        rot_acc_t<P>(nx, t, (bz * m) % p);
         reduce(nx, p);
         S = nx;
         m += 1;
@@ -451,7 +504,7 @@ __device__ __forceinline__ void group_direct(const ZpArgs& a, int mode, int s, u
       if (k <= a.N) wxor(Pa[WI], L);
       if (k != a.N) {
         if (ext && k < a.N) add_coeff(acc[WI], L, k, P);
-        else rot_acc(acc[WI], L, amt, P);
+        else rot_acc_t<P>(acc[WI], L, amt);
       }
     });
   }
@@ -467,7 +520,7 @@ __device__ __forceinline__ void group_direct(const ZpArgs& a, int mode, int s, u
   GroupWords<P, 0>::run([&](auto wc) {
     constexpr int WI = decltype(wc)::value;
     Word<NL> o[2];
-    finish_word<NL>(a, d, P, mode, ext, Pa[WI], acc[WI], o, grp * g + WI < W, bad);
+    finish_word<P>(a, d, mode, ext, Pa[WI], acc[WI], o, grp * g + WI < W, bad);
 #pragma unroll
     for (int q = 0; q < 2; q++)
       if (q < nout) group_put<P, WI>(ob[q], o[q]);
@@ -609,7 +662,7 @@ __global__ void __launch_bounds__(GT<P>::NT + 32, GT<P>::MINB) zp_generic_tma_ke
         Word<NL> L;
         group_word<P, WI>(buf, L);
         if (k <= a.N) wxor(Pa[WI], L);
-        if (k != a.N) rot_acc(acc[WI], L, amt, P);
+        if (k != a.N) rot_acc_t<P>(acc[WI], L, amt);
       });
       consumer_release(empty_sa + 8u * stage, lane);
       if (++stage == ST) { stage = 0; ph ^= 1u; }
@@ -626,7 +679,7 @@ __global__ void __launch_bounds__(GT<P>::NT + 32, GT<P>::MINB) zp_generic_tma_ke
     GroupWords<P, 0>::run([&](auto wc) {
       constexpr int WI = decltype(wc)::value;
       Word<NL> o[2];
-      finish_word<NL>(a, d, P, MODE, false, Pa[WI], acc[WI], o, true, bad);
+      finish_word<P>(a, d, MODE, false, Pa[WI], acc[WI], o, true, bad);
       group_put<P, WI>(ob[0], o[0]);
       group_put<P, WI>(ob[1], o[1]);
     });
