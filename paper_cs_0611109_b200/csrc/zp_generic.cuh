@@ -576,9 +576,14 @@ __global__ void __launch_bounds__(128, GP<P>::MINB) zp_generic_kernel(const __gr
 template <int P>
 struct GT {
   using GG = GP<P>;
-  static constexpr int NT = 128;                  // consumer threads = groups per tile
+  // consumer threads = groups per tile: 256 (2 CTAs, 18 warps per SM) while a group's g words of
+  // NL limbs stay at most 28 accumulator limbs, else 128 (3 CTAs; 2 from 20 limbs up).  Measured
+  // (c2 shape, 256 vs 128 threads): p = 67 ... 107 +10-20 % encode and recovery, p = 127 ... 163
+  // +4-17 % / +10-33 %, p = 211 (28 limbs) encode -4 %, recovery +19 %; p = 251 (32 limbs, spills)
+  // -30 %; 192 threads (14 warps) lose to both
+  static constexpr int NT = GG::NL * GG::g <= 28 ? 256 : 128;
   static constexpr int TB = NT * GG::GB;          // tile bytes
-  static constexpr int MINB = GG::NL * GG::g <= 20 ? 3 : 2;  // CTAs per SM (160 threads each)
+  static constexpr int MINB = NT >= 192 ? 2 : (GG::NL * GG::g <= 20 ? 3 : 2);  // CTAs per SM
   static constexpr int BUDGET = (227 * 1024) / MINB - 1024;
   static constexpr int ST_RAW = (BUDGET - 2 * TB - 128) / TB;
   static constexpr int ST = ST_RAW < 2 ? 2 : (ST_RAW > 8 ? 8 : ST_RAW);
