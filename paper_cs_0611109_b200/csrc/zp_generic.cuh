@@ -589,6 +589,7 @@ struct GT {
   static constexpr int ST = ST_RAW < 2 ? 2 : (ST_RAW > 8 ? 8 : ST_RAW);
   static constexpr size_t SMEM = static_cast<size_t>(ST + 2) * TB + 2 * ST * 8 + 16;
   static_assert(TB % 16 == 0, "TMA rows are multiples of 16 bytes");
+  static_assert(SMEM + 1024 <= 227 * 1024 / MINB + 1024, "MINB CTAs must fit the SM's shared memory");
 };
 
 template <int P, int MODE>

@@ -115,14 +115,31 @@ if g2:
                f"gpurun box, so not a scaling number): n_gpus {g2['n_gpus']}, {g2['ranks']['ranks_up']} ranks up, "
                f"per-rank ms {g2['per_rank_ms']}, verified {g2['verified']['ok']} "
                f"({g2['verified']['oracle_digest_stripes']}/{g2['verified']['oracle_digest_sampled']} oracle stripes).")
-pr = [(p, J(f"prime_p{p}"), J(f"prime_r01_p{p}")) for p in (73, 137, 241, 233)]
-pr = [x for x in pr if x[1]]
-if pr:
+x2 = J("next4_xgpu_dist2_gloo")
+if x2:
+    vv = x2["verified"]
     out.append("")
-    out.append("Large-word primes off the configs (c2 shape, N = 12, 4 MiB × 256; recovery of/at the measured copy rate, "
-               "round-1 library in brackets): " + ", ".join(
-                   f"p = {p} {a['kernels']['recover']['frac_of_peak']:.2f} ({b['kernels']['recover']['frac_of_peak']:.2f})"
-                   for p, a, b in pr if b) + ".")
+    out.append(f"NEXT-4 over the same self-launched path (`bench.py --gpus 2 --dist-backend gloo --xgpu 2`, two ranks "
+               f"sharing the gpurun box's GPU through CUDA IPC arenas, so not an NVLink number): {x2['ranks']['ranks_up']} "
+               f"ranks up, every rank verified (round trip {vv['mismatched_strip_digests']} strip digests off, poisoned "
+               f"recovery through the peer slots {vv['poisoned_recovery']['mismatched_strip_digests']} off over "
+               f"{vv['poisoned_recovery']['poisoned_bytes'] / 1e6:.0f} MB, fresh encode "
+               f"{vv['fresh_encode_mismatched_strip_digests']} off), oracle sample "
+               f"{vv.get('oracle_digest_stripes')}/{vv.get('oracle_digest_sampled')}.")
+pp = os.path.join(os.path.dirname(D.rstrip("/")), "r02_primes.json")
+if os.path.exists(pp):
+    with open(pp) as fh:
+        P = json.load(fh)["primes"]
+    fast = {int(p): v for p, v in P.items() if v and v["fast_path"]}
+    gen = {int(p): v for p, v in P.items() if v and not v["fast_path"]}
+    rng = lambda d, k: (min(v[k]["frac"] for v in d.values()), max(v[k]["frac"] for v in d.values()))  # noqa: E731
+    fe, fr, ge, gr = rng(fast, "encode"), rng(fast, "recover"), rng(gen, "encode"), rng(gen, "recover")
+    out.append("")
+    out.append(f"Every other prime (`profiles/r02_primes.json`, c2 shape N = 12, 4 MiB × 256, oracle-sampled lines; "
+               f"fraction of the measured copy rate): the {len(fast)} fast-path primes encode at {fe[0]:.2f}–{fe[1]:.2f} "
+               f"and recover at {fr[0]:.2f}–{fr[1]:.2f}; the {len(gen)} large-period primes on the TMA-staged generic "
+               f"kernel encode at {ge[0]:.2f}–{ge[1]:.2f} and recover at {gr[0]:.2f}–{gr[1]:.2f} (round 1: 0.27–0.40 / "
+               f"0.22–0.32).")
 out.append("\n### NEXT-1 (update / scrub)\n")
 out.append("| Config | Update kernel GB/s (of measured) | Scrub kernel GB/s (of measured) |")
 out.append("|---|---|---|")
