@@ -20,7 +20,8 @@ slim = args and args[0] == "--slim"
 if slim:
     args = args[1:]
 out, units, defines = args[0], args[1].split(), args[2:]
-B.build()  # main objects up to date
+if not os.environ.get("ZP_VARIANT_NO_MAIN"):  # (set: link against the main objects as they are)
+    B.build()  # main objects up to date
 tmp = os.path.join(ROOT, "build", "obj_variant")
 os.makedirs(tmp, exist_ok=True)
 for f in glob.glob(os.path.join(tmp, "*.o")):
