@@ -580,6 +580,16 @@ raid6c_status set_erasures(raid6c_plan plan, zp::ZpArgs& a, const raid6c_erasure
   return RAID6C_OK;
 }
 
+// True when every (host) erasure pair is {P, Q} = {N, N+1}, in either order.
+bool pq_only(int N, const raid6c_erasure* er, int count) {
+  if (count < 1) return false;
+  for (int s = 0; s < count; s++) {
+    const int i = std::min(er[s].lost_i, er[s].lost_j), j = std::max(er[s].lost_i, er[s].lost_j);
+    if (i != N || j != N + 1) return false;
+  }
+  return true;
+}
+
 // ------------------------------------------------------------------ cached single-stripe plans
 // The north-star calls share one plan per (device, p, N, bytes).  Callers hold the plan through
 // a shared_ptr for the whole call, so evicting an entry (the cache is bounded) only drops the
@@ -736,8 +746,9 @@ raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* cons
   a.ei = std::min(lost_i, lost_j);
   a.ej = std::max(lost_i, lost_j);
   std::unique_lock<std::mutex> lk(pl->mu);
-  if (pl->ext) a.prog = pl->d_prog;
-  st = launch(pl, a, zp::KMODE_RECOVER, nullptr);
+  const bool pq = a.ei == N && a.ej == N + 1;  // class PQ: the rebuild is the encode
+  if (pl->ext && !pq) a.prog = pl->d_prog;
+  st = launch(pl, a, pq ? zp::KMODE_ENCODE : zp::KMODE_RECOVER, nullptr);
   if (st != RAID6C_OK) return st;
   ZP_CUDA(cudaStreamSynchronize(nullptr));
   ZP_CUDA(cudaGetLastError());
@@ -761,6 +772,14 @@ raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t* data, size_t str
   if (st != RAID6C_OK) return st;
   if (!erasures) return RAID6C_E_NULL;
   DeviceGuard g(plan->device);
+  // Both parity strips lost in every stripe (class PQ, known on the host): the rebuild IS the
+  // encode (Eq. (znparity)), so it runs on the encode kernel (lighter geometry, 3 CTAs/SM where
+  // that wins) instead of the recovery kernel's PQ branch.
+  if (!erasures_on_device && pq_only(plan->N, erasures, num_erasures)) {
+    a.ei = plan->N;
+    a.ej = plan->N + 1;
+    return launch(plan, a, zp::KMODE_ENCODE, plan->stream);
+  }
   st = set_erasures(plan, a, erasures, num_erasures, erasures_on_device, num_stripes, true);
   if (st != RAID6C_OK) return st;
   return launch(plan, a, zp::KMODE_RECOVER, plan->stream);

@@ -151,6 +151,31 @@ def test_unaligned_pointers(offset):
             assert np.array_equal(_np(b.strip(s, j)), orig[j])
 
 
+@pytest.mark.parametrize("p,N", [(5, 4), (13, 12), (13, 17), (59, 20), (127, 9)])
+def test_pq_only_recovery_runs_as_encode(p, N):
+    """Launches whose every pair is {P, Q} (host list, either order; the single-stripe call) are
+    dispatched to the encode kernel: poisoned P and Q must come back equal to the oracle's."""
+    nbytes, S = 3 * 15360 + 333, 3
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=12, cfg=2)
+    plan = R.Plan(p, N, nbytes)
+    ref = []
+    for s in range(S):
+        data = synthetic.stripe_strips(12, 2, s, N, nbytes)
+        ref.append(oracle.encode_ext(p, data, nbytes) if N > p else oracle.encode(p, data, nbytes))
+    for pairs in ([(N, N + 1)], [(N + 1, N), (N, N + 1), (N + 1, N)]):
+        for s in range(S):
+            _poison(b, s, (N, N + 1))
+        plan.recover_strided(*b.args(), pairs)
+        plan.sync()
+        for s in range(S):
+            assert np.array_equal(_np(b.strip(s, N)), ref[s][0]), (p, N, pairs, s)
+            assert np.array_equal(_np(b.strip(s, N + 1)), ref[s][1]), (p, N, pairs, s)
+    _poison(b, 1, (N, N + 1))
+    R.recover(p, N, N + 1, N, [int(b.strip(1, k).data_ptr()) for k in range(N + 2)], nbytes)
+    assert np.array_equal(_np(b.strip(1, N)), ref[1][0]) and np.array_equal(_np(b.strip(1, N + 1)), ref[1][1])
+
+
 def test_lost_strips_never_read_and_neighbours_untouched():
     """Poisoned lost strips do not change the result; bytes outside the strips are untouched."""
     p, N, nbytes, S = 13, 12, 2 * 12288 + 77, 2
