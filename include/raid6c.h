@@ -148,7 +148,11 @@ raid6c_status raid6c_encode_strided(raid6c_plan plan, const uint8_t *data, size_
  * the strips named by erasures[s] (or erasures[0] for every stripe when num_erasures == 1)
  * are rebuilt from the other N strips of that stripe.  `erasures` is a HOST array when
  * erasures_on_device == 0, else a DEVICE array (already validated by the caller: each pair
- * distinct and in [0, N+2)).  Stripes may mix erasure classes (DD, DP, DQ, PQ). */
+ * distinct and in [0, N+2)).  Stripes may mix erasure classes (DD, DP, DQ, PQ).
+ * Kernel choice (results are identical): a HOST list whose every pair is {P, Q} runs as an
+ * encode (the PQ rebuild is Eq. (znparity) itself); a HOST list with no data-data pair runs
+ * on the light recovery kernel (DP / DQ / PQ epilogues only; fast path, N <= p); anything
+ * else, and every DEVICE list, on the full recovery kernel.  raid6c_recover chooses alike. */
 raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t *data, size_t strip_stride,
                                      size_t stripe_stride, uint8_t *P, uint8_t *Q,
                                      size_t parity_stride, int num_stripes,

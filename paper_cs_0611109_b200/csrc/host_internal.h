@@ -36,7 +36,7 @@ struct raid6c_plan_s {
   cudaStream_t stream = nullptr;
   const zp::FastEntry* fe = nullptr;
   int num_sms = 148;
-  int occ[6] = {1, 1, 1, 1, 1, 1};  // CTAs per SM per kernel mode
+  int occ[7] = {1, 1, 1, 1, 1, 1, 1};  // CTAs per SM per kernel mode
   bool ext = false;           // N > p: extended code of Eq. (qext)
   std::mutex mu;              // serialises the shared single-stripe plans' program buffer
   zp::ExtProg* d_prog = nullptr;

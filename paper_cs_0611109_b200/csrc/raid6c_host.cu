@@ -282,8 +282,9 @@ raid6c_status plan_init(raid6c_plan pl, int p, int N, size_t bytes, int device, 
   if (pl->fe && pl->ext && !pl->fe->kernel_ext[0]) pl->fe = nullptr;  // no fast extended kernels: generic
   if (pl->fe) {
     DeviceGuard g(device);
-    for (int m = 0; m < 6; m++) {
+    for (int m = 0; m < zp::NUM_KMODES; m++) {
       const void* k = pl->ext ? pl->fe->kernel_ext[m] : pl->fe->kernel[m];
+      if (!k) continue;  // (no extended light-recovery kernel)
       const size_t sm = pl->ext ? pl->fe->smem_ext[m] : pl->fe->smem_bytes[m];
       raid6c_status st = kernel_occupancy(device, k, pl->fe->threads[m] + 32, sm, &pl->occ[m]);
       if (st != RAID6C_OK) return st;
@@ -356,7 +357,7 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
       const bool small = (a.body_tiles + 1) * static_cast<uint64_t>(a.num_stripes) <=
                          static_cast<uint64_t>(pl->num_sms) * pl->occ[mode];
       if (aligned && !pl->ext && fe->partial_tile[mode] && pl->pbytes == pl->bytes && rest > 0 && rest % 16 == 0 &&
-          (mode == zp::KMODE_ENCODE || small)) {
+          (mode == zp::KMODE_ENCODE || mode == zp::KMODE_RECOVER_L || small)) {
         a.body_tiles += 1;
         a.last_tile = static_cast<uint32_t>(rest);
         a.tail_units_per_stripe = 0;
@@ -590,6 +591,14 @@ bool pq_only(int N, const raid6c_erasure* er, int count) {
   return true;
 }
 
+// True when no (host) erasure pair is class DD (every pair loses P or Q).
+bool no_dd(int N, const raid6c_erasure* er, int count) {
+  if (count < 1) return false;
+  for (int s = 0; s < count; s++)
+    if (std::max(er[s].lost_i, er[s].lost_j) < N) return false;
+  return true;
+}
+
 // ------------------------------------------------------------------ cached single-stripe plans
 // The north-star calls share one plan per (device, p, N, bytes).  Callers hold the plan through
 // a shared_ptr for the whole call, so evicting an entry (the cache is bounded) only drops the
@@ -748,7 +757,8 @@ raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* cons
   std::unique_lock<std::mutex> lk(pl->mu);
   const bool pq = a.ei == N && a.ej == N + 1;  // class PQ: the rebuild is the encode
   if (pl->ext && !pq) a.prog = pl->d_prog;
-  st = launch(pl, a, pq ? zp::KMODE_ENCODE : zp::KMODE_RECOVER, nullptr);
+  const bool light = !pq && pl->fe && !pl->ext && a.ej >= N;  // DP / DQ: light recovery kernel
+  st = launch(pl, a, pq ? zp::KMODE_ENCODE : (light ? zp::KMODE_RECOVER_L : zp::KMODE_RECOVER), nullptr);
   if (st != RAID6C_OK) return st;
   ZP_CUDA(cudaStreamSynchronize(nullptr));
   ZP_CUDA(cudaGetLastError());
@@ -782,7 +792,10 @@ raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t* data, size_t str
   }
   st = set_erasures(plan, a, erasures, num_erasures, erasures_on_device, num_stripes, true);
   if (st != RAID6C_OK) return st;
-  return launch(plan, a, zp::KMODE_RECOVER, plan->stream);
+  // No DD stripe in the launch (known on the host): the light recovery kernel (encode geometry;
+  // fast path, basic code)
+  const bool light = !erasures_on_device && plan->fe && !plan->ext && no_dd(plan->N, erasures, num_erasures);
+  return launch(plan, a, light ? zp::KMODE_RECOVER_L : zp::KMODE_RECOVER, plan->stream);
 }
 
 raid6c_status raid6c_scrub_strided(raid6c_plan plan, const uint8_t* data, size_t strip_stride, size_t stripe_stride,

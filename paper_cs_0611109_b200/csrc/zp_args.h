@@ -75,15 +75,16 @@ struct ZpArgs {
 struct FastEntry {
   int p;
   // per kernel mode (the geometry may differ between modes, see zp_fast.cuh Geo):
-  int chunk_bytes[6];  // bytes per thread-chunk (whole periods of lcm(n,32) bits)
-  int tile_bytes[6];   // TMA row bytes = consumer threads * chunk_bytes
-  int threads[6];      // consumer threads (+32 producer threads per CTA)
-  // __global__ void(ZpArgs) per mode: encode, recover, scrub, update, partial, combine (NEXT-4)
-  const void* kernel[6];
-  size_t smem_bytes[6];
-  int partial_tile[6];  // the mode's kernel loads / stores a partial last tile through TMA
-  const void* kernel_ext[6];  // extended-code (N > p) kernels, nullptr if p fails Theorem 25.3
-  size_t smem_ext[6];
+  int chunk_bytes[7];  // bytes per thread-chunk (whole periods of lcm(n,32) bits)
+  int tile_bytes[7];   // TMA row bytes = consumer threads * chunk_bytes
+  int threads[7];      // consumer threads (+32 producer threads per CTA)
+  // __global__ void(ZpArgs) per mode: encode, recover, scrub, update, partial, combine (NEXT-4),
+  // light recovery (classes DP / DQ / PQ only, encode geometry; basic code only)
+  const void* kernel[7];
+  size_t smem_bytes[7];
+  int partial_tile[7];  // the mode's kernel loads / stores a partial last tile through TMA
+  const void* kernel_ext[7];  // extended-code (N > p) kernels, nullptr if p fails Theorem 25.3
+  size_t smem_ext[7];
 };
 
 const FastEntry* fast_entry(int p);  // nullptr if p has no fast path
@@ -96,7 +97,8 @@ __host__ __device__ inline int pair_index(int x, int y, int N) {
 
 // Generic (runtime-p) kernels, any odd prime <= 257.
 enum : int { KMODE_ENCODE = 0, KMODE_RECOVER = 1, KMODE_SCRUB = 2, KMODE_UPDATE = 3, KMODE_PARTIAL = 4,
-             KMODE_COMBINE = 5 };
+             KMODE_COMBINE = 5, KMODE_RECOVER_L = 6 /* fast path, basic code: launches without DD */ };
+constexpr int NUM_KMODES = 7;
 cudaError_t generic_launch(const ZpArgs& a, int p, int mode, cudaStream_t st, int num_sms);
 
 }  // namespace zp

@@ -331,8 +331,11 @@ enum : int { CLS_PQ = 0, CLS_DQ = 1, CLS_DP = 2, CLS_DD = 3, CLS_SCRUB = 4, CLS_
 // rank, stored unsolved as partial syndromes (dP_r, dQ_r) into the word-range owners' slots.
 // MODE_COMBINE (NEXT-4): the owner of a word range folds the 2*nsrc partial rows of its slots
 // (row 2r = dP_r, row 2r+1 = dQ_r, already reduced) and runs the recovery epilogue.
-enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3, MODE_PARTIAL = 4, MODE_COMBINE = 5 };
-constexpr int NUM_MODES = 6;
+// MODE_RECOVER_L: recovery of launches without a DD stripe (classes DP, DQ, PQ: the epilogue is
+// one reduction and at most one rotation), built with the encode geometry and CTAs per SM
+enum : int { MODE_ENCODE = 0, MODE_RECOVER = 1, MODE_SCRUB = 2, MODE_UPDATE = 3, MODE_PARTIAL = 4, MODE_COMBINE = 5,
+             MODE_RECOVER_L = 6 };
+constexpr int NUM_MODES = 7;
 // Geometry of mode MODE's kernel for prime P (see Geo).
 // Recovery chunks of at least 15 lanes for p = 7, 13, 17 (measured r01: c2 recovery 0.96 -> 1.01
 // of the copy rate, p = 17 0.93 -> 0.98, p = 7 1.02 -> 1.05); not for p = 5 (config 1's 64 KiB
@@ -343,7 +346,7 @@ __host__ __device__ constexpr int recover_min_lanes() {
   return (P == 7 || P == 13 || P == 17) ? 15 : 12;
 }
 template <int P, int MODE>
-using GeoM = Geo<P, MODE == MODE_ENCODE || MODE == MODE_PARTIAL || MODE == MODE_COMBINE,
+using GeoM = Geo<P, MODE == MODE_ENCODE || MODE == MODE_RECOVER_L || MODE == MODE_PARTIAL || MODE == MODE_COMBINE,
                  MODE == MODE_RECOVER ? recover_min_lanes<P>() : 12, MODE == MODE_RECOVER>;
 constexpr int K_NEW = -1;     // row index of the update's new-data buffer
 constexpr int K_PART_P = -2;  // partial-mode outputs (slots of the word-range owners)
@@ -371,7 +374,7 @@ __device__ __forceinline__ ItemDesc item_desc(const ZpArgs& a, int s) {
     return d;
   } else {
     int i = a.N, j = a.N + 1;
-    if constexpr (MODE == MODE_RECOVER || MODE == MODE_PARTIAL || MODE == MODE_COMBINE) {
+    if constexpr (MODE == MODE_RECOVER || MODE == MODE_RECOVER_L || MODE == MODE_PARTIAL || MODE == MODE_COMBINE) {
       if (a.er) {
         const int2 e = a.er[static_cast<int64_t>(s) * a.er_stride];
         i = e.x; j = e.y;
@@ -832,7 +835,7 @@ __device__ __forceinline__ uint32_t count_nonzero_words(const uint32_t (&V)[G::C
 }
 
 // Class epilogue: produces the two output chunks and their strip indices.
-template <class G>
+template <class G, bool DD = true>
 __device__ __forceinline__ void finish(const ZpArgs& a, const ItemDesc& d, uint32_t (&Pa)[G::C], Acc<G>& acc,
                                        const uint2* __restrict__ mtab, uint32_t (&o0)[G::C], uint32_t (&o1)[G::C],
                                        int& k0, int& k1) {
@@ -848,12 +851,12 @@ __device__ __forceinline__ void finish(const ZpArgs& a, const ItemDesc& d, uint3
     rot_acc<G>(o0, d.x, mtab, acc);
     reduce<G>(acc, o1);
     k0 = d.x; k1 = a.N + 1;
-  } else if (d.cls == CLS_DP) {  // d_j = x^{-j}(Q + sum_{k!=j} x^k d_k); P = sum
+  } else if (!DD || d.cls == CLS_DP) {  // d_j = x^{-j}(Q + sum_{k!=j} x^k d_k); P = sum
     reduce<G>(acc, o0);
 #pragma unroll
     for (int l = 0; l < C; l++) o1[l] = Pa[l] ^ o0[l];
     k0 = d.x; k1 = a.N;
-  } else {  // DD: d_y = (1+x^z)^{-1}(dP + x^{-x} dQ), d_x = d_y + dP
+  } else if constexpr (DD) {  // DD: d_y = (1+x^z)^{-1}(dP + x^{-x} dQ), d_x = d_y + dP
     uint32_t t[C];
     reduce_plus<G>(acc, Pa, t);
     // d_y = S_M t with S_M = sum_{m<M} b^m, b = x^{2z}, M = (p+1)/2 (reading R11)
@@ -897,7 +900,8 @@ __device__ __forceinline__ void build_mtab(uint2* mtab) {
 // (spills at 128 / 72 registers for p = 59 / 61, a 63-register cap for the 8 KiB-tile primes).
 template <int P, int MODE>
 __host__ __device__ constexpr int min_blocks() {
-  return ((P == 7 || P == 13 || P == 257) && (MODE == MODE_ENCODE || MODE == MODE_PARTIAL || MODE == MODE_UPDATE))
+  return ((P == 7 || P == 13 || P == 257) &&
+          (MODE == MODE_ENCODE || MODE == MODE_RECOVER_L || MODE == MODE_PARTIAL || MODE == MODE_UPDATE))
              ? 3 : 2;
 }
 
@@ -931,7 +935,7 @@ __host__ __device__ constexpr bool has_partial_tile() {
 #ifdef ZP_NO_PARTIAL_TILE  // A/B control
   return false;
 #else
-  return (32 % (P - 1) == 0) && (MODE == MODE_ENCODE || MODE == MODE_RECOVER) && !EXT;
+  return (32 % (P - 1) == 0) && (MODE == MODE_ENCODE || MODE == MODE_RECOVER || MODE == MODE_RECOVER_L) && !EXT;
 #endif
 }
 
@@ -969,7 +973,7 @@ __device__ __forceinline__ void epilogue(const ZpArgs& a, const ItemDesc& d, int
   } else if constexpr (EXT) {
     finish_ext<G>(a, d, s, Pa, acc, mtab, o0, o1, k0, k1);
   } else {
-    finish<G>(a, d, Pa, acc, mtab, o0, o1, k0, k1);
+    finish<G, MODE != MODE_RECOVER_L>(a, d, Pa, acc, mtab, o0, o1, k0, k1);
   }
 }
 
@@ -1060,7 +1064,7 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
     }
     // (words that straddle lanes; for lane-aligned words, n | 32, the generic row loop measured
     // faster: c1 encode / recovery -5 / -8 % with fold_item)
-    if constexpr ((MODE == MODE_ENCODE || MODE == MODE_RECOVER) && !EXT && (32 % G::n != 0)) {
+    if constexpr ((MODE == MODE_ENCODE || MODE == MODE_RECOVER || MODE == MODE_RECOVER_L) && !EXT && (32 % G::n != 0)) {
       fold_item<G, ST>(a, d, my_stages, full_sa, empty_sa, mtab, lane, stage, ph, Pa, acc);
     } else if constexpr ((MODE == MODE_ENCODE || MODE == MODE_RECOVER) && EXT && (32 % G::n != 0)) {
       fold_item_ext<G, ST>(a, d, my_stages, full_sa, empty_sa, mtab, lane, stage, ph, Pa, acc);
@@ -1088,7 +1092,7 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
     int k0 = 0, k1 = 0, k2 = 0;
     epilogue<EMODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
 #ifdef ZP_NOOP_RECOVER  // negative control of bench.py's verification: recovery stores nothing
-    if constexpr (MODE == MODE_RECOVER) continue;
+    if constexpr (MODE == MODE_RECOVER || MODE == MODE_RECOVER_L) continue;
 #endif
     if constexpr (NOUT > 0) {
       if constexpr (MODE != MODE_UPDATE) {  // (update waited at the start of the item)
@@ -1162,7 +1166,7 @@ __global__ void __launch_bounds__(GeoM<P, MODE>::THREADS + 32, (Layout<P, MODE>:
     } else {
       epilogue<EMODE, G, true, EXT>(a, d, s, Pa, acc, NEW, mtab, o0, o1, k0, k1, k2);
 #ifdef ZP_NOOP_RECOVER
-      if constexpr (MODE == MODE_RECOVER) continue;
+      if constexpr (MODE == MODE_RECOVER || MODE == MODE_RECOVER_L) continue;
 #endif
       st_chunk_global<C>(out_ptr(a, k0, s, off), off, row_len(a, k0), o0);
       st_chunk_global<C>(out_ptr(a, k1, s, off), off, row_len(a, k1), o1);
@@ -1191,6 +1195,8 @@ FastEntry make_entry() {
   fill_geo<P, 0>(e);
   e.kernel[MODE_ENCODE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_ENCODE>);
   e.kernel[MODE_RECOVER] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_RECOVER>);
+  e.kernel[MODE_RECOVER_L] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_RECOVER_L>);
+  e.smem_bytes[MODE_RECOVER_L] = Layout<P, MODE_RECOVER_L>::SMEM;
   e.kernel[MODE_SCRUB] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_SCRUB>);
   e.kernel[MODE_UPDATE] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_UPDATE>);
   e.kernel[MODE_PARTIAL] = reinterpret_cast<const void*>(&zp_kernel<P, MODE_PARTIAL>);
@@ -1226,6 +1232,7 @@ FastEntry make_entry() {
   namespace zp {                                                                             \
   template __global__ void zp_kernel<PP, MODE_ENCODE>(const __grid_constant__ ZpArgs);        \
   template __global__ void zp_kernel<PP, MODE_RECOVER>(const __grid_constant__ ZpArgs);       \
+  template __global__ void zp_kernel<PP, MODE_RECOVER_L>(const __grid_constant__ ZpArgs);     \
   template __global__ void zp_kernel<PP, MODE_SCRUB>(const __grid_constant__ ZpArgs);         \
   template __global__ void zp_kernel<PP, MODE_UPDATE>(const __grid_constant__ ZpArgs);        \
   template __global__ void zp_kernel<PP, MODE_PARTIAL>(const __grid_constant__ ZpArgs);       \

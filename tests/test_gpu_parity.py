@@ -176,6 +176,41 @@ def test_pq_only_recovery_runs_as_encode(p, N):
     assert np.array_equal(_np(b.strip(1, N)), ref[1][0]) and np.array_equal(_np(b.strip(1, N + 1)), ref[1][1])
 
 
+@pytest.mark.parametrize("p,N,nbytes", [(3, 2, 65536), (5, 4, 65536), (5, 4, 3 * 10752 + 77), (13, 12, 4 * 15360 + 333),
+                                        (17, 16, 2 * 13440 + 1008), (59, 58, 2 * 14848 + 5), (61, 60, 15360 + 1),
+                                        (257, 64, 3 * 8192 + 96), (233, 30, 14848 + 700)])
+def test_light_recovery_dp_dq_batches(p, N, nbytes):
+    """Launches with no DD stripe (host pair lists of DP / DQ / PQ) run on the light recovery
+    kernel: every rebuilt strip must equal the generator's / the oracle's bytes."""
+    S = 5
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=21, cfg=4)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    orig = []
+    for s in range(S):
+        data = synthetic.stripe_strips(21, 4, s, N, nbytes)
+        P, Q = oracle.encode(p, data, nbytes)
+        assert np.array_equal(_np(b.strip(s, N)), P) and np.array_equal(_np(b.strip(s, N + 1)), Q)
+        orig.append(data + [P, Q])
+    mixes = [[(N - 1, N)] * S, [(0, N + 1)] * S,
+             [(s % N, N + (s % 2)) for s in range(S)], [(N, N + 1), (N + 1, 1), (2 % N, N), (N, N + 1), (N + 1, 0)]]
+    for pairs in mixes:
+        for s, (i, j) in enumerate(pairs):
+            _poison(b, s, (i, j))
+        plan.recover_strided(*b.args(), pairs if len(set(pairs)) > 1 else pairs[:1])
+        plan.sync()
+        for s, (i, j) in enumerate(pairs):
+            for k in (i, j):
+                assert np.array_equal(_np(b.strip(s, k)), orig[s][k]), (p, N, pairs, s, k)
+    for (i, j) in [(1, N), (N + 1, N - 1)]:  # the single-stripe call
+        _poison(b, 2, (i, j))
+        R.recover(p, N, i, j, [int(b.strip(2, k).data_ptr()) for k in range(N + 2)], nbytes)
+        for k in (i, j):
+            assert np.array_equal(_np(b.strip(2, k)), orig[2][k]), (p, N, i, j, k)
+
+
 def test_lost_strips_never_read_and_neighbours_untouched():
     """Poisoned lost strips do not change the result; bytes outside the strips are untouched."""
     p, N, nbytes, S = 13, 12, 2 * 12288 + 77, 2
