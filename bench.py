@@ -334,7 +334,14 @@ def run_ours(args):
         plan.encode_strided(*enc_args)
     total_steps = args.warmup + args.steps
     pair_lists = [pair_schedule(args.config, N, S, stripe0, t) for t in range(total_steps)]
-    pair_dev = [torch.tensor(pl, dtype=torch.int32, device=dev) for pl in pair_lists]
+    # where the per-stripe pair table lives when recover_strided is called: on the device (used in
+    # place, the default) or on the host (uploaded by the call inside the timed region: measured
+    # -1.7 % on c1's 0.27 ms launches, nothing on c2 / c5, profiles/r02e/split_ab.txt)
+    pairs_mode = args.pairs
+    if pairs_mode == "host":
+        pair_dev = [R.erasure_array(pl) for pl in pair_lists]  # marshalled once, outside the timed region
+    else:
+        pair_dev = [torch.tensor(pl, dtype=torch.int32, device=dev) for pl in pair_lists]
     torch.cuda.synchronize(dev)
 
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(total_steps)]
@@ -483,7 +490,8 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u32 (bitwise GF(2) words)",
         "data": "synthetic (seeded SplitMix64 counter generator, generated on device)",
         "config": {"workload": c["desc"], "p": p, "N": N, "strip_bytes": nbytes, "parity_bytes": pb,
-                   "stripes_per_gpu": S, "ops": ops, "parallelism": f"stripe-sharded x{world} (no data-path collective)",
+                   "stripes_per_gpu": S, "ops": ops, "pairs": pairs_mode if do_rec else None,
+                   "parallelism": f"stripe-sharded x{world} (no data-path collective)",
                    "l2": "working set >= 1 GiB >> 126 MB L2 (no flush needed)"},
         "roofline": roof, "kernels": per_kernel, "gpu_launches": launches, "clocks": clk,
         "per_rank_ms": per_rank_ms, "ranks": rank_info,
@@ -1493,6 +1501,8 @@ def main():
     ap.add_argument("--xgpu", type=int, default=0,
                     help="NEXT-4: spread each stripe's strips over G ranks (emulated on one GPU at --gpus 1)")
     ap.add_argument("--sweep", action="store_true", help="config 3 strip-size sweep 64 KiB -> 16 MiB")
+    ap.add_argument("--pairs", default="device", choices=["host", "device"],
+                    help="per-stripe erasure table passed to recover_strided from the host or the device")
     ap.add_argument("--no-verify", dest="verify", action="store_false")
     ap.add_argument("--no-oracle-check", dest="oracle_check", action="store_false")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")

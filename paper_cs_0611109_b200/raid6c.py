@@ -149,10 +149,16 @@ def recover(p: int, N: int, lost_i: int, lost_j: int, strips, nbytes: int) -> No
 
 
 def _erasure_array(pairs):
+    """Host erasure pairs as a ctypes array of raid6c_erasure (a prebuilt one passes through)."""
+    if isinstance(pairs, ctypes.Array) and getattr(pairs, "_type_", None) is Erasure:
+        return pairs
     arr = (Erasure * len(pairs))()
     for s, (i, j) in enumerate(pairs):
         arr[s].lost_i, arr[s].lost_j = int(i), int(j)
     return arr
+
+
+erasure_array = _erasure_array  # marshal a host pair list once, reuse it across calls
 
 
 def fill(dst, strip_stride: int, stripe_stride: int, nbytes: int, nstrips: int, nstripes: int, seed: int,

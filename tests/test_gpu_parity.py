@@ -211,6 +211,46 @@ def test_light_recovery_dp_dq_batches(p, N, nbytes):
             assert np.array_equal(_np(b.strip(2, k)), orig[2][k]), (p, N, i, j, k)
 
 
+@pytest.mark.parametrize("p,N,nbytes,S,dd_every", [(5, 4, 65536, 400, 0), (13, 12, 4 * 15360 + 333, 480, 3),
+                                                   (61, 60, 3 * 15360 + 16, 640, 3)])
+def test_large_mixed_host_table_batches(p, N, nbytes, S, dd_every):
+    """Mixed-class batches from HOST pair tables, large enough that every CTA of the persistent
+    launch walks several items of different classes (a raw list, then a prebuilt raid6c_erasure
+    array; pairs in either index order).  Every lost strip is poisoned first; afterwards every
+    byte of the batch must equal the pre-erasure snapshot (untouched neighbours included), and on
+    stripes spread over the batch the data the generator's bytes and the parity the oracle's."""
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=33, cfg=1)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    snap_d, snap_p = b.data.clone(), b.par.clone()
+    allp = synthetic.all_pairs(N)
+    dd = [pr for pr in allp if pr[1] < N]
+    li = [pr for pr in allp if pr[1] >= N]
+    if dd_every == 0:   # the bench's c1 schedule: cycle through every pair (6 of 15 are data-data)
+        pairs = [allp[(s + 37) % len(allp)] for s in range(S)]
+    else:               # every dd_every-th stripe data-data
+        pairs = [dd[(7 * s) % len(dd)] if s % dd_every == 0 else li[(5 * s) % len(li)] for s in range(S)]
+        pairs = [(j, i) if s % 2 else (i, j) for s, (i, j) in enumerate(pairs)]
+    for rep in range(2):  # twice: the second call rewrites the plan's device table behind the first
+        for s, (i, j) in enumerate(pairs):
+            _poison(b, s, (i, j))
+        n0 = R.launch_count()
+        plan.recover_strided(*b.args(), pairs if rep == 0 else R.erasure_array(pairs))
+        plan.sync()
+        assert R.launch_count() - n0 == 1
+        assert torch.equal(b.data, snap_d) and torch.equal(b.par, snap_p)
+    sample = sorted(set(list(range(0, S, max(1, S // 10))) + [S - 1, S - 2, 1]))
+    for s in sample:
+        data = synthetic.stripe_strips(33, 1, s, N, nbytes)
+        P, Q = oracle.encode(p, data, nbytes)
+        ref = data + [P, Q]
+        for k in range(N + 2):
+            assert np.array_equal(_np(b.strip(s, k)), ref[k]), (p, s, k, pairs[s])
+    plan.close()
+
+
 def test_lost_strips_never_read_and_neighbours_untouched():
     """Poisoned lost strips do not change the result; bytes outside the strips are untouched."""
     p, N, nbytes, S = 13, 12, 2 * 12288 + 77, 2
