@@ -57,7 +57,7 @@ typedef enum {
     RAID6C_OK = 0,
     RAID6C_E_INVALID_P = 1,     /* p is not an odd prime in [3, 257] */
     RAID6C_E_INVALID_N = 2,     /* N < 1, N > 2p-1, or p < N with p failing Theorem 25.3 */
-    RAID6C_E_INVALID_INDEX = 3, /* lost index outside [0, N+2) or lost_i == lost_j */
+    RAID6C_E_INVALID_INDEX = 3, /* lost index outside [0, N+2) (lost_j: or RAID6C_NONE), or lost_i == lost_j */
     RAID6C_E_NULL = 4,          /* a required pointer is NULL */
     RAID6C_E_SIZE = 5,          /* bytes == 0, num_stripes < 0, or a stride smaller than its strip */
     RAID6C_E_CUDA = 6,          /* CUDA runtime / launch error (sticky; see raid6c_last_cuda_error) */
@@ -65,7 +65,15 @@ typedef enum {
     RAID6C_E_PLAN = 8           /* plan/call mismatch (p, N or bytes differ from the plan) */
 } raid6c_status;
 
-/* One erasure pair per stripe for batched recovery (either order; -1 is not allowed). */
+/* lost_j of a SINGLE erasure (the optional case of SPEC.md:441): only strip lost_i is lost.  The
+ * library runs it as the pair (lost_i, Q) -- (P, Q) when lost_i is Q -- i.e. a lost data strip is
+ * the XOR of the other data strips and P (Eq. (znparity), row 1), and the pair's parity strip is
+ * regenerated from the data: the caller must let that INTACT parity strip be rewritten (with the
+ * bytes it already holds when the stripe was consistent).  Accepted in HOST arguments only. */
+#define RAID6C_NONE (-1)
+
+/* One erasure pair per stripe for batched recovery (either order; lost_j may be RAID6C_NONE in a
+ * HOST array, never in a DEVICE array). */
 typedef struct {
     int32_t lost_i;
     int32_t lost_j;
@@ -127,7 +135,8 @@ raid6c_status raid6c_sync(raid6c_plan plan);
  * completed, with its status. */
 raid6c_status raid6c_encode(int p, int N, const uint8_t *const *strips, uint8_t *P, uint8_t *Q, size_t bytes);
 
-/* Rebuild lost strips lost_i and lost_j (any order) of one stripe (Lemma 23.2,
+/* Rebuild lost strips lost_i and lost_j (any order; lost_j = RAID6C_NONE: lost_i alone, see
+ * RAID6C_NONE for the parity strip that is rewritten with it) of one stripe (Lemma 23.2,
  * PAPER.md:370-406; Sec. 4.6).  strips: HOST array of N+2 DEVICE
  * pointers, 0..N-1 data (`bytes`), N = P, N+1 = Q (parity_bytes).  The two lost strips are
  * written, the rest read.  Synchronous. */

@@ -94,6 +94,7 @@ void plan_release(raid6c_plan pl);
 raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st);
 raid6c_status launch_combine(raid6c_plan pl, zp::ZpArgs& a, cudaStream_t st);
 raid6c_status check_erasure(int N, int i, int j);
+void pair_of_single(int N, int i, int& j);  // lost_j == RAID6C_NONE -> the pair the library runs
 raid6c_status strided_args(raid6c_plan pl, const uint8_t* data, size_t strip_stride, size_t stripe_stride,
                            const uint8_t* P, const uint8_t* Q, size_t parity_stride, int num_stripes,
                            zp::ZpArgs& a);

@@ -68,7 +68,8 @@ raid6c_status host_run(raid6c_plan pl, uint8_t* data, size_t strip_stride, size_
     if (num_erasures != 1 && num_erasures != num_stripes) return RAID6C_E_SIZE;
     pairs.resize(num_stripes);
     for (int s = 0; s < num_stripes; s++) {
-      const raid6c_erasure& e = er[num_erasures == 1 ? 0 : s];
+      raid6c_erasure e = er[num_erasures == 1 ? 0 : s];
+      pair_of_single(pl->N, e.lost_i, e.lost_j);
       raid6c_status c = check_erasure(pl->N, e.lost_i, e.lost_j);
       if (c != RAID6C_OK) return c;
       pairs[s] = make_int2(std::min(e.lost_i, e.lost_j), std::max(e.lost_i, e.lost_j));

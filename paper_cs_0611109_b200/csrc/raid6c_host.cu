@@ -385,6 +385,21 @@ raid6c_status launch(raid6c_plan pl, zp::ZpArgs& a, int mode, cudaStream_t st) {
   return tables_after_read(pl, a, st);
 }
 
+// Single erasure (lost_j == RAID6C_NONE, host arguments): the pair (i, Q), or (P, Q) for i = Q.
+void pair_of_single(int N, int i, int& j) {
+  if (j == RAID6C_NONE) j = (i == N + 1) ? N : N + 1;
+}
+
+// A copy of a host erasure list with its single erasures completed to pairs (false: none found).
+bool complete_singles(int N, const raid6c_erasure* er, int count, std::vector<raid6c_erasure>& out) {
+  bool any = false;
+  for (int s = 0; s < count; s++) any |= er[s].lost_j == RAID6C_NONE;
+  if (!any) return false;
+  out.assign(er, er + count);
+  for (auto& e : out) pair_of_single(N, e.lost_i, e.lost_j);
+  return true;
+}
+
 raid6c_status check_erasure(int N, int i, int j) {
   if (i == j || i < 0 || j < 0 || i >= N + 2 || j >= N + 2) return RAID6C_E_INVALID_INDEX;
   return RAID6C_OK;
@@ -739,6 +754,7 @@ raid6c_status raid6c_recover(int p, int N, int lost_i, int lost_j, uint8_t* cons
   if (!is_valid_p(p)) return RAID6C_E_INVALID_P;
   if (N < 1 || N > 2 * p - 1 || (N > p && !ext_supported_p(p))) return RAID6C_E_INVALID_N;
   if (bytes == 0) return RAID6C_E_SIZE;
+  pair_of_single(N, lost_i, lost_j);
   raid6c_status st = check_erasure(N, lost_i, lost_j);
   if (st != RAID6C_OK) return st;
   if (!strips) return RAID6C_E_NULL;
@@ -781,6 +797,9 @@ raid6c_status raid6c_recover_strided(raid6c_plan plan, uint8_t* data, size_t str
   raid6c_status st = strided_args(plan, data, strip_stride, stripe_stride, P, Q, parity_stride, num_stripes, a);
   if (st != RAID6C_OK) return st;
   if (!erasures) return RAID6C_E_NULL;
+  std::vector<raid6c_erasure> completed;  // single erasures (RAID6C_NONE) as pairs
+  if (!erasures_on_device && num_erasures >= 1 && complete_singles(plan->N, erasures, num_erasures, completed))
+    erasures = completed.data();
   DeviceGuard g(plan->device);
   // Both parity strips lost in every stripe (class PQ, known on the host): the rebuild IS the
   // encode (Eq. (znparity)), so it runs on the encode kernel (lighter geometry, 3 CTAs/SM where

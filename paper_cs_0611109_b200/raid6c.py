@@ -81,6 +81,9 @@ STATUS = {0: "RAID6C_OK", 1: "RAID6C_E_INVALID_P", 2: "RAID6C_E_INVALID_N", 3: "
           4: "RAID6C_E_NULL", 5: "RAID6C_E_SIZE", 6: "RAID6C_E_CUDA", 7: "RAID6C_E_NO_DEVICE", 8: "RAID6C_E_PLAN"}
 
 
+NONE = -1  # RAID6C_NONE: lost_j of a single erasure (host arguments only)
+
+
 class Raid6Error(RuntimeError):
     def __init__(self, status: int, where: str):
         self.status = status
@@ -143,7 +146,8 @@ def encode(p: int, N: int, strips, P, Q, nbytes: int) -> None:
 
 
 def recover(p: int, N: int, lost_i: int, lost_j: int, strips, nbytes: int) -> None:
-    """raid6c_recover: strips = N+2 device tensors/addresses (0..N-1 data, N = P, N+1 = Q)."""
+    """raid6c_recover: strips = N+2 device tensors/addresses (0..N-1 data, N = P, N+1 = Q).
+    lost_j = NONE: strip lost_i alone (runs as the pair (lost_i, Q), or (P, Q) for lost_i = Q)."""
     arr = (_vp * (N + 2))(*[_ptr(s) for s in strips])
     _check(_lib.raid6c_recover(p, N, lost_i, lost_j, arr, nbytes), "raid6c_recover")
 

@@ -298,6 +298,66 @@ def test_host_buffer_api_matches_device_path():
     assert torch.equal(hd, ref_d) and torch.equal(hp[:, :, :b.pb], ref_p[:, :, :b.pb])
 
 
+@pytest.mark.parametrize("p,N,nbytes", [(5, 4, 2 * 10752 + 1024), (13, 12, 2 * 15360 + 333), (257, 20, 8192 + 96),
+                                        (67, 9, 5000), (5, 9, 4096 + 7)])
+def test_single_erasure(p, N, nbytes):
+    """lost_j = RAID6C_NONE (optional): strip lost_i alone is rebuilt -- as the pair
+    (lost_i, Q), or (P, Q) for lost_i = Q -- through the single-stripe call, a host pair table and
+    the host-buffer call; every strip of the stripe must then hold the generator's data and the
+    oracle's parity (fast, generic and extended-code plans)."""
+    S = 3
+    b = Batch(p, N, nbytes, S)
+    b.fill_synthetic(seed=44, cfg=2)
+    plan = R.Plan(p, N, nbytes)
+    plan.encode_strided(*b.args())
+    plan.sync()
+    enc = oracle.encode_ext if N > p else oracle.encode
+    ref = []
+    for s in range(S):
+        data = synthetic.stripe_strips(44, 2, s, N, nbytes)
+        P, Q = enc(p, data, nbytes)
+        ref.append(data + [P, Q])
+
+    def check(tag):
+        for s in range(S):
+            for k in range(N + 2):
+                assert np.array_equal(_np(b.strip(s, k)), ref[s][k]), (p, N, tag, s, k)
+
+    check("encode")
+    for i in range(N + 2):  # the single-stripe call, every strip of stripe 1
+        _poison(b, 1, (i,))
+        R.recover(p, N, i, R.NONE, [int(b.strip(1, k).data_ptr()) for k in range(N + 2)], nbytes)
+        check(("single", i))
+    tables = [[(s % (N + 2), R.NONE) for s in range(S)],                      # singles only
+              [(N + 1, R.NONE), (0, N - 1) if N > 1 else (0, N), (N, R.NONE)],  # mixed with a pair
+              [(N - 1, R.NONE)]]                                              # one entry for every stripe
+    for t in tables:
+        full = t if len(t) == S else t * S
+        for s, (i, j) in enumerate(full):
+            _poison(b, s, (i,) if j == R.NONE else (i, j))
+        plan.recover_strided(*b.args(), t)
+        plan.sync()
+        check(("table", t))
+    # the host-buffer call
+    hd = b.data.cpu().pin_memory()
+    hp = b.par.cpu().pin_memory()
+    hd[0, 0, :nbytes] = 0xA5
+    hp[1, 1, :b.pb] = 0xA5
+    hd[2, N - 1, :nbytes] = 0xA5
+    plan.recover_host(hd, b.ss, N * b.ss, hp, int(hp.data_ptr()) + b.ps, 2 * b.ps, S,
+                      [(0, R.NONE), (N + 1, R.NONE), (N - 1, R.NONE)])
+    plan.sync()
+    for s in range(S):
+        for k in range(N + 2):
+            got = hd[s, k, :nbytes].numpy() if k < N else hp[s, k - N, :b.pb].numpy()
+            assert np.array_equal(got, ref[s][k]), (p, N, "host", s, k)
+    with pytest.raises(R.Raid6Error, match="INVALID_INDEX"):
+        plan.recover_strided(*b.args(), [(R.NONE, 0)])   # lost_i must name a strip
+    with pytest.raises(R.Raid6Error, match="INVALID_INDEX"):
+        plan.recover_strided(*b.args(), [(0, -2)])
+    plan.close()
+
+
 # ------------------------------------------------------------------ argument errors (T1)
 def test_argument_errors_are_synchronous():
     t = torch.zeros(64, dtype=torch.uint8, device="cuda")
