@@ -153,6 +153,13 @@ def _free_port():
     return port
 
 
+def _dist_on(world):
+    """The process group is up: more than one rank, or RAID6C_FORCE_DIST=1 (a 1-rank group under
+    torchrun, so that the NCCL plumbing itself -- init with device_id, object gathers, barriers,
+    device-tensor collectives -- runs on a one-GPU box; tests/test_gpu_multirank.py)."""
+    return world > 1 or os.environ.get("RAID6C_FORCE_DIST") == "1"
+
+
 def self_launch(args):
     """--gpus N (N > 1) without a torchrun environment: bring the N ranks up ourselves (one process
     per GPU through torch.distributed.run on 127.0.0.1) and return their exit status.  Never falls
@@ -188,7 +195,7 @@ def init_ranks(args):
     local = local % torch.cuda.device_count()  # (only differs in the 1-GPU multi-rank rehearsal)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if _dist_on(world):
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:  # gloo: rehearse the multi-rank path with several ranks on one GPU (host-side collectives only)
@@ -196,17 +203,17 @@ def init_ranks(args):
     props = torch.cuda.get_device_properties(dev)
     me = {"rank": rank, "cuda_device": local, "uuid": str(getattr(props, "uuid", ""))[:13], "pid": os.getpid()}
     info = [me]
-    if world > 1:
+    if _dist_on(world):
         info = [None] * world
         dist.all_gather_object(info, me)
     return rank, world, local, dev, {"ranks_up": len(info), "distinct_gpus": len({i["uuid"] for i in info}),
-                                     "backend": args.dist_backend if world > 1 else None, "ranks": info}
+                                     "backend": args.dist_backend if _dist_on(world) else None, "ranks": info}
 
 
 def gather_dict(d):
     """Union of per-rank dicts on every rank (all_gather_object; identity at world size 1)."""
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return dict(d)
     parts = [None] * dist.get_world_size()
     dist.all_gather_object(parts, d)
@@ -362,7 +369,7 @@ def run_ours(args):
     # snapshot for verification after the timed region (recovery rewrites lost strips in place)
     ref_data, ref_par = (data.clone(), par.clone()) if args.verify else (None, None)
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if _dist_on(world):
         dist.barrier()
     torch.cuda.synchronize(dev)
     clocks = ClockSampler(local)
@@ -505,7 +512,7 @@ def run_ours(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.close()
-    if world > 1:
+    if _dist_on(world):
         dist.barrier()
         dist.destroy_process_group()
     if verified is not None and not verified["ok"]:
@@ -702,7 +709,7 @@ def run_full(args):
     bad_total.zero_()
     wave_digests.clear()
     torch.cuda.synchronize(dev)
-    if world > 1:
+    if _dist_on(world):
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -778,7 +785,7 @@ def run_full(args):
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.close()
-    if world > 1:
+    if _dist_on(world):
         dist.barrier()
         dist.destroy_process_group()
     if not line["verified"]["ok"]:
@@ -1331,7 +1338,7 @@ def run_e2e(args, R, torch, plan, data, par, S, N, nbytes, pb, ss, ps, pair_list
     steps = max(1, args.e2e_steps)
     times, h2d, d2h = [], 0, 0
     for t in range(1 + steps):
-        if world > 1:
+        if _dist_on(world):
             import torch.distributed as dist
             dist.barrier()
         t0 = time.perf_counter()

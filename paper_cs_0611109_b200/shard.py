@@ -22,7 +22,7 @@ def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar (e.g. elapsed ms) over the default process group."""
     import torch
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -39,7 +39,7 @@ def sum_over_ranks(values, device=None) -> list[int]:
     """Elementwise sum of per-rank integer counters over the default process group."""
     import torch
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return [int(v) for v in values]
     t = torch.tensor([int(v) for v in values], dtype=torch.int64, device=_coll_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -50,7 +50,7 @@ def gather_over_ranks(value: float, device=None) -> list[float]:
     """Per-rank values of a scalar (e.g. each rank's elapsed ms), in rank order."""
     import torch
     import torch.distributed as dist
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+    if not (dist.is_available() and dist.is_initialized()):
         return [float(value)]
     dev = _coll_device(device)
     t = torch.tensor([float(value)], dtype=torch.float64, device=dev)

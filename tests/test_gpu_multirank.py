@@ -27,6 +27,30 @@ def _bench(*args, timeout=900):
     return json.loads(lines[0]), r.stderr
 
 
+def test_nccl_plumbing_on_one_rank():
+    """The NCCL path itself (never reached by the gloo rehearsals): a ONE-rank process group forced
+    with RAID6C_FORCE_DIST=1 runs init_process_group("nccl", device_id=...), the object gathers, the
+    barriers around the timed region and the device-tensor collectives of shard.py on the box's
+    GPU, for the bench step and for a whole-config (--full) run."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ, RAID6C_FORCE_DIST="1", RANK="0", WORLD_SIZE="1", LOCAL_RANK="0",
+               MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    for extra in (["--stripes", "16", "--steps", "2", "--e2e-steps", "1"], ["--full", "--config", "4", "--stripes", "8"]):
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1", "--warmup", "3", "--oracle-stripes", "2",
+               *extra]
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+        assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        assert len(lines) == 1, r.stdout[-3000:]
+        d = json.loads(lines[0])
+        assert d["n_gpus"] == 1 and d["ranks"]["backend"] == "nccl" and d["ranks"]["ranks_up"] == 1
+        assert d["verified"]["ok"] and ("--full" in extra or len(d["per_rank_ms"]) == 1)
+
+
 def test_self_launch_two_ranks():
     d, err = _bench("--gpus", "2", "--dist-backend", "gloo", "--config", "2", "--stripes", "8", "--steps", "2",
                     "--warmup", "3", "--no-e2e", "--oracle-stripes", "4")
