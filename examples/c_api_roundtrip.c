@@ -98,6 +98,17 @@ int main(int argc, char** argv) {
     for (int k = 0; k < 2; k++)
       bad += memcmp(h_chk + (size_t)s * 2 * ps + (size_t)k * ps, h_par + (size_t)s * 2 * ps + (size_t)k * ps, pb) != 0;
 
+  /* a single lost strip: lost_j = RAID6C_NONE (runs as the pair (lost_i, Q): d_0 of stripe 0 is
+   * rebuilt from the other strips and P, and the intact Q is regenerated with it) */
+  CHECK_C(cudaMemset(d_data, 0xA5, bytes));
+  raid6c_erasure one = {0, RAID6C_NONE};
+  CHECK_R(raid6c_recover_strided(plan, d_data, ss, (size_t)N * ss, d_par, d_par + ps, 2 * ps, 1, &one, 1, 0));
+  CHECK_R(raid6c_sync(plan));
+  CHECK_C(cudaMemcpy(h_chk, d_data, bytes, cudaMemcpyDeviceToHost));
+  bad += memcmp(h_chk, h_data, bytes) != 0;
+  CHECK_C(cudaMemcpy(h_chk, d_par + ps, pb, cudaMemcpyDeviceToHost));
+  bad += memcmp(h_chk, h_par + ps, pb) != 0;
+
   /* an argument error is synchronous and has no side effect */
   raid6c_erasure badpair = {0, 0};
   const raid6c_status e = raid6c_recover_strided(plan, d_data, ss, (size_t)N * ss, d_par, d_par + ps, 2 * ps, 1,

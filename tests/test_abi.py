@@ -75,6 +75,22 @@ def test_no_device_is_reported_not_faked():
         R.encode(13, 1, [0], 0, 0, 16)  # NULL pointers are rejected before any device call
 
 
+def test_single_erasure_argument_checks_need_no_device():
+    """lost_j = RAID6C_NONE is completed on the host before any device call: a bad lost_i is still
+    an index error, and a well-formed single erasure gets past the index check (to the NULL-strip
+    check here), with or without a GPU."""
+    assert R.NONE == -1
+    null4 = [0, 0, 0, 0]
+    for bad_i in (-1, 4, 7):
+        with pytest.raises(R.Raid6Error, match="INVALID_INDEX"):
+            R.recover(5, 2, bad_i, R.NONE, null4, 16)
+    with pytest.raises(R.Raid6Error, match="INVALID_INDEX"):
+        R.recover(5, 2, 0, -2, null4, 16)
+    for i in range(4):
+        with pytest.raises(R.Raid6Error, match="E_NULL"):
+            R.recover(5, 2, i, R.NONE, null4, 16)
+
+
 def test_build_and_shard_import_without_library():
     """A fresh checkout has no libraid6c.so: the build module (which makes it) and the host
     sharding logic must import, while the binding itself must fail loudly (no fallback)."""
