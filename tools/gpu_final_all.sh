@@ -22,7 +22,7 @@ for spec in "2 16 zp --prime 17" "2 16 rs --prime 17" "2 12 zp" "2 12 rs" "4 58 
   run next3_c$1_N$2_$3${4:+_p17} 600 --config $1 --data-strips $2 --code $3 $4 $5 --no-e2e --no-cpu-baseline; done
 for spec in "4 8" "5 8" "2 4" "2 8" "1 4" "3 8"; do set -- $spec; run next4_xgpu_c$1_G$2 600 --config $1 --xgpu $2; done
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29655 \
-  bench.py --xgpu 2 --dist-backend gloo --config 2 --stripes 32 > $O/next4_xgpu_ipc2.log 2>&1; echo "ipc2 rc=$?"
+  bench.py --gpus 2 --xgpu 2 --dist-backend gloo --config 2 --stripes 32 > $O/next4_xgpu_ipc2.log 2>&1; echo "ipc2 rc=$?"
 grep '^{' $O/next4_xgpu_ipc2.log | tail -1 > $O/next4_xgpu_ipc2.json
 run impl_reference 600 --impl reference
 # ncu: launch list of the default workload (2 timed steps) and a full-set capture of its encode + recover
