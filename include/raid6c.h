@@ -69,7 +69,9 @@ typedef enum {
  * library runs it as the pair (lost_i, Q) -- (P, Q) when lost_i is Q -- i.e. a lost data strip is
  * the XOR of the other data strips and P (Eq. (znparity), row 1), and the pair's parity strip is
  * regenerated from the data: the caller must let that INTACT parity strip be rewritten (with the
- * bytes it already holds when the stripe was consistent).  Accepted in HOST arguments only. */
+ * bytes it already holds when the stripe was consistent).  Accepted in the HOST arguments of
+ * raid6c_recover, raid6c_recover_strided and raid6c_recover_host; every other call, and a DEVICE
+ * array, must name two strips (RAID6C_E_INVALID_INDEX otherwise, where the library can see it). */
 #define RAID6C_NONE (-1)
 
 /* One erasure pair per stripe for batched recovery (either order; lost_j may be RAID6C_NONE in a
